@@ -1,0 +1,138 @@
+/*
+ * b64_oracle.c -- plain scalar CPU oracle for base64 encode / validating decode.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code, header, table or constant generator with the CUDA path
+ * (paper_1704_00605_b200/csrc), and the CUDA path never calls it.
+ *
+ * It is a transcription of the paper's Algorithm 1 and Algorithm 2
+ * (W. Mula, D. Lemire, "Faster Base64 Encoding and Decoding using AVX2
+ * Instructions", /root/reference/PAPER.md), in the paper's order and
+ * notation, with the readings listed in DESIGN.md §3:
+ *
+ *   R-alphabet  B and A are defined by the ranges of P:184-185 (Table I's
+ *               body is missing), cross-checked by Table II
+ *                and Table III in the tests.
+ *   R-pad       '=' is structural, never a data value: it is acceptable only
+ *               in the last two positions of an input whose length is a
+ *               multiple of 4, and a '=' in position m-2 forces '=' in
+ *               position m-1.
+ *   R2          the reported error offset is the first position that cannot
+ *               continue any valid encoding (left-to-right scan).
+ *   R-length    m not divisible by 4 (Alg 2 requires it): status
+ *               LENGTH at offset 4*floor(m/4) unless an earlier position is
+ *               unacceptable.
+ *   R-noncanon  non-canonical trailing bits are accepted.
+ *
+ * Built with -O2 -fno-tree-vectorize -fno-tree-slp-vectorize so that it
+ * stays the plain scalar baseline.  Parity pins: tests/test_oracle.py.
+ */
+#include <stddef.h>
+#include <stdint.h>
+
+#define ORACLE_OK 0
+#define ORACLE_INVALID_CHAR 1
+#define ORACLE_LENGTH 2
+
+/* B: 6-bit value -> ASCII (Table I: A..Z, a..z, 0..9, '+', '/'). */
+int oracle_B(int v) {
+  if (v >= 0 && v <= 25) return 'A' + v;
+  if (v >= 26 && v <= 51) return 'a' + (v - 26);
+  if (v >= 52 && v <= 61) return '0' + (v - 52);
+  if (v == 62) return '+';
+  if (v == 63) return '/';
+  return -1;
+}
+
+/* A: ASCII -> 6-bit value, negative for a character outside Table I
+ * (Alg 2 preamble).  '=' is NOT given a value here (reading R-pad);
+ * Alg 2's "'=' has value 0" convention is applied only when the final quad
+ * is emitted, below. */
+int oracle_A(int ch) {
+  if (ch >= 'A' && ch <= 'Z') return ch - 'A';
+  if (ch >= 'a' && ch <= 'z') return ch - 'a' + 26;
+  if (ch >= '0' && ch <= '9') return ch - '0' + 52;
+  if (ch == '+') return 62;
+  if (ch == '/') return 63;
+  return -1;
+}
+
+int64_t oracle_encoded_len(int64_t n) { return 4 * ((n + 2) / 3); }
+
+/* Algorithm 1.  p must hold 4*ceil(n/3) bytes.  Returns the
+ * number of characters written. */
+int64_t oracle_encode(const uint8_t *s, int64_t n, uint8_t *p) {
+  int64_t o = 0;
+  int64_t i;
+  /* for i in 0, 3, ..., n - (n mod 3) - 3 */
+  for (i = 0; i + 3 <= n - (n % 3); i += 3) {
+    p[o++] = (uint8_t)oracle_B(s[i] / 4);
+    p[o++] = (uint8_t)oracle_B(((s[i] * 16) % 64) + (s[i + 1] / 16));
+    p[o++] = (uint8_t)oracle_B(((s[i + 1] * 4) % 64) + (s[i + 2] / 64));
+    p[o++] = (uint8_t)oracle_B(s[i + 2] % 64);
+  }
+  i = n - n % 3;
+  if (i < n) {
+    p[o++] = (uint8_t)oracle_B(s[i] / 4);
+    if (i == n - 1) {
+      p[o++] = (uint8_t)oracle_B((s[i] * 16) % 64);
+      p[o++] = '=';
+    } else if (i == n - 2) {
+      p[o++] = (uint8_t)oracle_B(((s[i] * 16) % 64) + (s[i + 1] / 16));
+      p[o++] = (uint8_t)oracle_B((s[i + 1] * 4) % 64);
+    }
+    p[o++] = '=';
+  }
+  return o;
+}
+
+/* Reading R-pad / R2: is position i of c[0..m) acceptable? */
+static int acceptable(const uint8_t *c, int64_t m, int64_t i) {
+  const int in_alphabet = oracle_A(c[i]) >= 0;
+  if (m % 4 == 0 && i == m - 1)
+    return (in_alphabet || c[i] == '=') && (c[m - 2] != '=' || c[i] == '=');
+  if (m % 4 == 0 && i == m - 2) return in_alphabet || c[i] == '=';
+  return in_alphabet;
+}
+
+/* Algorithm 2 with readings R-pad, R2, R-length.
+ * p must hold 3*floor(m/4) bytes.  Returns the status; *out_len receives the
+ * number of bytes appended to p, *err_pos the error offset or -1. */
+int oracle_decode(const uint8_t *c, int64_t m, uint8_t *p, int64_t *out_len,
+                  int64_t *err_pos) {
+  int64_t o = 0;
+  const int64_t q = m / 4;
+  int64_t i;
+  *err_pos = -1;
+  /* for i in 0, 4, ..., n - 4 */
+  for (i = 0; i + 4 <= 4 * q; i += 4) {
+    int j;
+    int a, b, cc, d;
+    /* "if any of a, b, c, d is negative: report an error",
+     * first offending byte (R2) */
+    for (j = 0; j < 4; ++j) {
+      if (!acceptable(c, m, i + j)) {
+        *err_pos = i + j;
+        *out_len = o;
+        return ORACLE_INVALID_CHAR;
+      }
+    }
+    /* a..d <- A(C_i..C_{i+3}); '=' contributes 0 */
+    a = c[i] == '=' ? 0 : oracle_A(c[i]);
+    b = c[i + 1] == '=' ? 0 : oracle_A(c[i + 1]);
+    cc = c[i + 2] == '=' ? 0 : oracle_A(c[i + 2]);
+    d = c[i + 3] == '=' ? 0 : oracle_A(c[i + 3]);
+    p[o++] = (uint8_t)((a * 4) + (b / 16));
+    if (c[i + 2] == '=') break;
+    p[o++] = (uint8_t)(((b * 16) % 256) + (cc / 4));
+    if (c[i + 3] == '=') break;
+    p[o++] = (uint8_t)(((cc * 64) % 256) + d);
+  }
+  *out_len = o;
+  if (m % 4 != 0) { /* R-length (P:156 requires n divisible by 4) */
+    *err_pos = 4 * q;
+    return ORACLE_LENGTH;
+  }
+  return ORACLE_OK;
+}
