@@ -1,0 +1,171 @@
+/*
+ * b64gpu.h -- C ABI of libb64gpu.so: base64 encode / validating decode on B200.
+ *
+ * Paper: W. Mula, D. Lemire, "Faster Base64 Encoding and Decoding using AVX2
+ * Instructions" (arXiv 1704.00605); "P:n" = line n of /root/reference/PAPER.md.
+ * Design and the readings of ambiguous passages: DESIGN.md.
+ *
+ * Conventions (all entry points)
+ *  - Pointers named d_* are CUDA device pointers (any alignment is legal; the
+ *    16-byte aligned case is the fast path).  h_* are host pointers.
+ *  - Sizes and offsets are int64_t.  Error offsets are 0-based byte indexes
+ *    into the input; -1 means "no error".
+ *  - `stream` is a cudaStream_t (0 = legacy default stream).  Every call only
+ *    enqueues work on `stream` unless it says it synchronizes.
+ *  - The caller owns every buffer; the library allocates nothing on the hot
+ *    path except a small per-(device, stream) scratch record created on the
+ *    first decode call on that stream (16 B of device memory plus 32 B of
+ *    mapped pinned host memory; never freed).  Do not make the first decode
+ *    call on a stream inside CUDA-graph capture.
+ *  - Input and output buffers must not overlap.
+ *  - Return codes: >= 0 success (or a length), negative = b64_status error.
+ *    Nothing is launched when an argument check fails.  No exceptions cross
+ *    the ABI; nothing is printed.
+ *  - Reads: the kernels read input through 16-byte aligned windows, so up to
+ *    15 bytes before d_in and after d_in + n that share a 16-byte granule
+ *    with the input may be read (never written).  Torch / cudaMalloc
+ *    allocations are padded to at least 256 B, so this never leaves the
+ *    allocation in practice.
+ *  - All entry points are reentrant for calls on distinct streams.
+ */
+#ifndef B64GPU_H
+#define B64GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *b64_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  B64_OK = 0,               /* valid input, fully decoded                            */
+  B64_ERR_INVALID_CHAR = 1, /* a byte outside the alphabet / misplaced '=' */
+  B64_ERR_LENGTH = 2,       /* m not divisible by 4 (Alg 2 requires it)        */
+  B64_ERR_ARG = -1,         /* bad argument; nothing launched                          */
+  B64_ERR_CUDA = -2,        /* a CUDA runtime call failed                              */
+  B64_ERR_WORKSPACE = -3    /* batched workspace too small                             */
+} b64_status;
+
+/* Device-side result record of one decode (16-byte aligned). */
+typedef struct {
+  int64_t out_len;   /* bytes of valid output (see b64_decode)             */
+  int64_t err_pos;   /* first error offset, -1 if none                      */
+  int32_t status;    /* b64_status (0, 1 or 2)                              */
+  int32_t pad_count; /* number of trailing '=' consumed (0, 1, 2)           */
+} b64_result;
+
+/* ------------------------------------------------------------------ sizes */
+
+/* 4*ceil(n/3): encoded length of n bytes with '=' padding (P:116-119,
+ * Alg 1).  Pure host; -1 if n < 0. */
+int64_t b64_encoded_len(int64_t n);
+
+/* 3*floor(m/4): output capacity a decode of m characters may write
+ * (Alg 2 emits at most 3 bytes per complete quad). -1 if m < 0. */
+int64_t b64_decoded_max_len(int64_t m);
+
+/* ----------------------------------------------------------------- encode */
+
+/* Algorithm 1 on n bytes at d_in: writes exactly
+ * b64_encoded_len(n) ASCII characters of the standard alphabet
+ * to d_out, '=' padded, no line breaks.  Asynchronous on `stream`.
+ * Returns the output length, or B64_ERR_ARG / B64_ERR_CUDA. */
+int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t stream);
+
+/* ----------------------------------------------------------------- decode */
+
+/* Validating decode, Algorithm 2 with DESIGN.md readings
+ * R-pad / R2 / R-length, of m characters at d_in into d_out (capacity
+ * b64_decoded_max_len(m)).  Enqueues on `stream` and then SYNCHRONIZES the
+ * stream.  On return:
+ *   OK:            *out_len = 3*(m/4) - pad_count, *err_pos = -1
+ *   INVALID_CHAR:  *err_pos = first offending byte (minimum over the whole
+ *                  buffer), *out_len = 3*floor(err_pos/4); d_out[0..out_len)
+ *                  holds the complete quads before it, later bytes are
+ *                  unspecified (within capacity)
+ *   LENGTH:        m % 4 != 0 and no earlier error: *err_pos = 4*floor(m/4),
+ *                  *out_len = 3*floor(m/4)
+ * Returns the status (>= 0) or a negative error code.  out_len / err_pos may
+ * be NULL. */
+int b64_decode(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *out_len,
+               int64_t *err_pos, b64_stream_t stream);
+
+/* Fully asynchronous decode: same semantics as b64_decode, the result record
+ * is written by the device to d_result (device or mapped host memory, 8-byte
+ * aligned) when the kernel finishes.  Returns B64_OK if enqueued. */
+int b64_decode_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, b64_result *d_result,
+                     b64_stream_t stream);
+
+/* Decode of one shard of a larger buffer split on 4-character boundaries
+ * (multi-GPU sharder).  final_shard != 0: identical to
+ * b64_decode_async.  final_shard == 0: m must be a multiple of 4 and the
+ * final-quad padding rule is NOT applied ('=' anywhere is an error), because
+ * a later shard follows.  Offsets in d_result are shard-relative. */
+int b64_decode_shard_async(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
+                           b64_result *d_result, b64_stream_t stream);
+
+/* ---------------------------------------------------------------- batched */
+
+/* Scratch bytes (device memory, 256-byte aligned) that a batched call over k
+ * messages totalling at most total_in bytes of input needs.
+ * direction: 0 = encode, 1 = decode. */
+size_t b64_batch_workspace_bytes(int64_t k, int64_t total_in, int direction);
+
+/* Batched encode of k independent messages: message i is
+ * d_in[d_in_off[i] .. d_in_off[i+1]) (d_in_off: k+1 non-decreasing int64 on
+ * the device, d_in_off[0] may be > 0).  Writes d_out_off[0..k] (device,
+ * d_out_off[0] = 0, d_out_off[i+1]-d_out_off[i] = b64_encoded_len(len_i))
+ * and each encoding contiguously to d_out.  Messages are split into tiles
+ * assigned to CTAs by the prefix sums of their lengths (BASELINE.json
+ * north_star).  d_ws: b64_batch_workspace_bytes(k, total_in, 0) bytes,
+ * total_in >= d_in_off[k] - d_in_off[0].  Asynchronous. */
+int b64_encode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                     uint8_t *d_out, int64_t *d_out_off, void *d_ws, size_t ws_bytes,
+                     b64_stream_t stream);
+
+/* Batched validating decode: message i is decoded independently under the
+ * rules of b64_decode.  d_out_off[i+1]-d_out_off[i] reserves the nominal
+ * decoded length 3*floor(len_i/4) - p_i (p_i = number of trailing '=' in the
+ * last two characters when len_i % 4 == 0), so outputs of valid messages are
+ * contiguous.  Per message (device arrays of k): d_out_len[i], d_err_pos[i]
+ * (message-relative, -1 if none), d_status[i] (b64_status >= 0).
+ * Asynchronous. */
+int b64_decode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                     uint8_t *d_out, int64_t *d_out_off, int64_t *d_out_len, int64_t *d_err_pos,
+                     int32_t *d_status, void *d_ws, size_t ws_bytes, b64_stream_t stream);
+
+/* ------------------------------------------------------------ host buffers */
+
+/* End-to-end helpers with HOST buffers (pinned memory recommended): the
+ * input is copied host->device in chunks, each chunk is processed as soon as
+ * it lands and its output copied back, so transfers overlap the kernels.
+ * d_scratch_in / d_scratch_out are device buffers of at least
+ * n (resp. m) and b64_encoded_len(n) (resp. b64_decoded_max_len(m)) bytes.
+ * Both synchronize `stream` before returning. */
+int64_t b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, uint8_t *d_scratch_in,
+                        uint8_t *d_scratch_out, b64_stream_t stream);
+int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out_len,
+                    int64_t *err_pos, uint8_t *d_scratch_in, uint8_t *d_scratch_out,
+                    b64_stream_t stream);
+
+/* ------------------------------------------------------------------ misc */
+
+/* Unit-aligned shard [*begin, *end) of a buffer of `total` bytes for rank
+ * `rank` of `world` (unit = 3 for encode input, 4 for decode input): the
+ * Q = ceil(total/unit) units are split as [floor(r*Q/G), floor((r+1)*Q/G)),
+ * so only the last rank sees a partial unit.  Pure host. */
+int b64_shard(int64_t total, int unit, int world, int rank, int64_t *begin, int64_t *end);
+
+/* Static string for a status code. */
+const char *b64_status_str(int status);
+
+/* Library version string and the sm architecture it was compiled for. */
+const char *b64_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B64GPU_H */

@@ -1,0 +1,305 @@
+"""ctypes binding of libb64gpu.so: same names as include/b64gpu.h.
+
+Argument marshalling only (tensor -> pointer, stream -> handle, status ->
+exception).  Nothing here computes base64.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libb64gpu.so")
+
+B64_OK = 0
+B64_ERR_INVALID_CHAR = 1
+B64_ERR_LENGTH = 2
+B64_ERR_ARG = -1
+B64_ERR_CUDA = -2
+B64_ERR_WORKSPACE = -3
+
+# Every symbol include/b64gpu.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "b64_encoded_len", "b64_decoded_max_len", "b64_encode", "b64_decode",
+    "b64_decode_async", "b64_decode_shard_async", "b64_batch_workspace_bytes",
+    "b64_encode_batch", "b64_decode_batch", "b64_encode_host", "b64_decode_host",
+    "b64_shard", "b64_status_str", "b64_build_info",
+)
+
+_lib = None
+
+
+class B64Error(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        super().__init__(f"{what}: {b64_status_str(code)} ({code})")
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [("out_len", ctypes.c_int64), ("err_pos", ctypes.c_int64),
+                ("status", ctypes.c_int32), ("pad_count", ctypes.c_int32)]
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libb64gpu.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "b64_encoded_len": (i64, [i64]),
+        "b64_decoded_max_len": (i64, [i64]),
+        "b64_encode": (i64, [vp, i64, vp, vp]),
+        "b64_decode": (i32, [vp, i64, vp, p64, p64, vp]),
+        "b64_decode_async": (i32, [vp, i64, vp, vp, vp]),
+        "b64_decode_shard_async": (i32, [vp, i64, i32, vp, vp, vp]),
+        "b64_batch_workspace_bytes": (sz, [i64, i64, i32]),
+        "b64_encode_batch": (i32, [vp, vp, i64, i64, vp, vp, vp, sz, vp]),
+        "b64_decode_batch": (i32, [vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "b64_encode_host": (i64, [vp, i64, vp, vp, vp, vp]),
+        "b64_decode_host": (i32, [vp, i64, vp, p64, p64, vp, vp, vp]),
+        "b64_shard": (i32, [i64, i32, i32, i32, p64, p64]),
+        "b64_status_str": (ctypes.c_char_p, [i32]),
+        "b64_build_info": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+# ------------------------------------------------------------ helpers ---
+
+def _ptr(t) -> int | None:
+    return t.data_ptr() if t is not None else None
+
+
+def _stream(stream, device):
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _check_u8_cuda(t, name):
+    import torch
+
+    if not (isinstance(t, torch.Tensor) and t.dtype == torch.uint8 and t.is_cuda and t.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous uint8 CUDA tensor")
+
+
+# --------------------------------------------------------------- sizes ---
+
+def b64_encoded_len(n: int) -> int:
+    return load_library().b64_encoded_len(n)
+
+
+def b64_decoded_max_len(m: int) -> int:
+    return load_library().b64_decoded_max_len(m)
+
+
+def b64_status_str(code: int) -> str:
+    return load_library().b64_status_str(code).decode()
+
+
+def b64_build_info() -> str:
+    return load_library().b64_build_info().decode()
+
+
+# -------------------------------------------------------------- encode ---
+
+def b64_encode(inp, out=None, stream=None):
+    """Encode the uint8 CUDA tensor ``inp``; returns the output view."""
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    lib = load_library()
+    n = inp.numel()
+    need = lib.b64_encoded_len(n)
+    if out is None:
+        out = torch.empty(max(need, 1), dtype=torch.uint8, device=inp.device)
+    else:
+        _check_u8_cuda(out, "out")
+        if out.numel() < need:
+            raise ValueError("out too small")
+    rc = lib.b64_encode(_ptr(inp), n, _ptr(out), _stream(stream, inp.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_encode")
+    return out[:rc]
+
+
+# -------------------------------------------------------------- decode ---
+
+def b64_decode(inp, out=None, stream=None):
+    """Validating decode (synchronizes the stream).
+
+    Returns (out_view, status, err_pos); out_view has out_len bytes."""
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    lib = load_library()
+    m = inp.numel()
+    cap = lib.b64_decoded_max_len(m)
+    if out is None:
+        out = torch.empty(max(cap, 1), dtype=torch.uint8, device=inp.device)
+    else:
+        _check_u8_cuda(out, "out")
+        if out.numel() < cap:
+            raise ValueError("out too small")
+    ol = ctypes.c_int64(0)
+    ep = ctypes.c_int64(0)
+    st = lib.b64_decode(_ptr(inp), m, _ptr(out), ctypes.byref(ol), ctypes.byref(ep),
+                        _stream(stream, inp.device))
+    if st < 0:
+        raise B64Error(st, "b64_decode")
+    return out[: ol.value], st, ep.value
+
+
+def result_tensor(device):
+    """A device tensor holding one b64_result record (int64[3])."""
+    import torch
+
+    return torch.zeros(3, dtype=torch.int64, device=device)
+
+
+def unpack_result(res):
+    """(out_len, err_pos, status, pad_count) from a result tensor."""
+    v = res.cpu().tolist()
+    st = v[2] & 0xFFFFFFFF
+    pc = (v[2] >> 32) & 0xFFFFFFFF
+    return v[0], v[1], st, pc
+
+
+def b64_decode_async(inp, out, result, stream=None):
+    return b64_decode_shard_async(inp, out, result, final_shard=True, stream=stream)
+
+
+def b64_decode_shard_async(inp, out, result, final_shard=True, stream=None):
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    _check_u8_cuda(out, "out")
+    if not (result.is_cuda and result.dtype == torch.int64 and result.numel() >= 3):
+        raise TypeError("result must be an int64[3] CUDA tensor")
+    lib = load_library()
+    m = inp.numel()
+    if out.numel() < lib.b64_decoded_max_len(m):
+        raise ValueError("out too small")
+    rc = lib.b64_decode_shard_async(_ptr(inp), m, 1 if final_shard else 0, _ptr(out),
+                                    result.data_ptr(), _stream(stream, inp.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_decode_shard_async")
+
+
+# ------------------------------------------------------------- batched ---
+
+def b64_batch_workspace_bytes(k: int, total_in: int, direction: int) -> int:
+    return load_library().b64_batch_workspace_bytes(k, total_in, direction)
+
+
+def _ws(k, total, direction, device, ws):
+    import torch
+
+    need = b64_batch_workspace_bytes(k, total, direction)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need + 256, dtype=torch.uint8, device=device)
+    # 256-byte alignment (torch allocations are 512-aligned; views may not be)
+    off = (-ws.data_ptr()) % 256
+    return ws[off:], need
+
+
+def b64_encode_batch(inp, in_off, out=None, out_off=None, ws=None, total_in=None, stream=None):
+    """Batched encode; in_off: int64[k+1] CUDA tensor.  Returns (out, out_off)."""
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    k = in_off.numel() - 1
+    total = inp.numel() if total_in is None else total_in
+    if out is None:
+        out = torch.empty(max(4 * ((total + 2) // 3) + 4 * k, 1), dtype=torch.uint8, device=inp.device)
+    if out_off is None:
+        out_off = torch.empty(k + 1, dtype=torch.int64, device=inp.device)
+    w, need = _ws(k, total, 0, inp.device, ws)
+    rc = load_library().b64_encode_batch(_ptr(inp), in_off.data_ptr(), k, total, _ptr(out),
+                                         out_off.data_ptr(), w.data_ptr(), w.numel(),
+                                         _stream(stream, inp.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_encode_batch")
+    return out, out_off
+
+
+def b64_decode_batch(inp, in_off, out=None, out_off=None, out_len=None, err_pos=None,
+                     status=None, ws=None, total_in=None, stream=None):
+    """Batched validating decode.  Returns (out, out_off, out_len, err_pos, status)."""
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    k = in_off.numel() - 1
+    dev = inp.device
+    total = inp.numel() if total_in is None else total_in
+    if out is None:
+        out = torch.empty(max(3 * (total // 4) + 1, 1), dtype=torch.uint8, device=dev)
+    if out_off is None:
+        out_off = torch.empty(k + 1, dtype=torch.int64, device=dev)
+    if out_len is None:
+        out_len = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
+    if err_pos is None:
+        err_pos = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
+    if status is None:
+        status = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    w, need = _ws(k, total, 1, dev, ws)
+    rc = load_library().b64_decode_batch(_ptr(inp), in_off.data_ptr(), k, total, _ptr(out),
+                                         out_off.data_ptr(), out_len.data_ptr(), err_pos.data_ptr(),
+                                         status.data_ptr(), w.data_ptr(), w.numel(),
+                                         _stream(stream, dev))
+    if rc < 0:
+        raise B64Error(rc, "b64_decode_batch")
+    return out, out_off, out_len[:k], err_pos[:k], status[:k]
+
+
+# -------------------------------------------------------- host buffers ---
+
+def b64_encode_host(h_in, h_out, d_scratch_in, d_scratch_out, stream=None):
+    """h_in/h_out: (pinned) CPU uint8 tensors; returns the output length."""
+    lib = load_library()
+    n = h_in.numel()
+    rc = lib.b64_encode_host(_ptr(h_in), n, _ptr(h_out), _ptr(d_scratch_in), _ptr(d_scratch_out),
+                             _stream(stream, d_scratch_in.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_encode_host")
+    return rc
+
+
+def b64_decode_host(h_in, h_out, d_scratch_in, d_scratch_out, stream=None):
+    """Returns (status, out_len, err_pos)."""
+    lib = load_library()
+    ol = ctypes.c_int64(0)
+    ep = ctypes.c_int64(0)
+    st = lib.b64_decode_host(_ptr(h_in), h_in.numel(), _ptr(h_out), ctypes.byref(ol),
+                             ctypes.byref(ep), _ptr(d_scratch_in), _ptr(d_scratch_out),
+                             _stream(stream, d_scratch_in.device))
+    if st < 0:
+        raise B64Error(st, "b64_decode_host")
+    return st, ol.value, ep.value
+
+
+# -------------------------------------------------------------- shards ---
+
+def b64_shard(total: int, unit: int, world: int, rank: int) -> tuple[int, int]:
+    b = ctypes.c_int64(0)
+    e = ctypes.c_int64(0)
+    rc = load_library().b64_shard(total, unit, world, rank, ctypes.byref(b), ctypes.byref(e))
+    if rc < 0:
+        raise B64Error(rc, "b64_shard")
+    return b.value, e.value

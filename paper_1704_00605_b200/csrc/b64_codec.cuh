@@ -1,0 +1,275 @@
+// b64_codec.cuh -- per-thread / per-tile base64 arithmetic for the sm_100a
+// kernels (device code only).  Paper rows: SURVEY.md §8 a2-a3 (encode regroup
+// + alphabet map), a8-a10 (decode classify/translate, first-error reduction,
+// pack).  No code is shared with oracle/.
+#pragma once
+#include <cstdint>
+
+namespace b64 {
+
+// ------------------------------------------------------------ geometry ---
+constexpr int kWarpsC = 8;                  // compute warps per CTA
+constexpr int kNT = kWarpsC * 32;           // compute threads per CTA
+constexpr int kThreads = kNT + 32;          // + one producer (TMA) warp
+constexpr int kStagesIn = 4;                // input ring depth
+constexpr int kStagesOut = 2;               // output staging depth
+
+// Encode: each compute thread turns 12 bytes (4 groups) into 16 chars per pass.
+constexpr int kEncPasses = 2;
+constexpr int kEncIn = kNT * 12 * kEncPasses;   // 6144 input bytes per tile
+constexpr int kEncOut = kNT * 16 * kEncPasses;  // 8192 output chars per tile
+// Decode: each compute thread turns 16 chars (4 quads) into 12 bytes per pass.
+constexpr int kDecPasses = 2;
+constexpr int kDecIn = kNT * 16 * kDecPasses;   // 8192 input chars per tile
+constexpr int kDecOut = kNT * 12 * kDecPasses;  // 6144 output bytes per tile
+
+constexpr int round_up_c(int x, int a) { return (x + a - 1) / a * a; }
+
+constexpr uint8_t kInvalid = 0xFF;  // decode-table marker for bytes outside the alphabet
+constexpr int kFlagFinal = 1;       // tile holds the final quad of a padded-able stream
+
+// Tile descriptor: produced arithmetically (single buffer) or by the batch
+// planner, handed from the producer warp to the compute warps through smem.
+struct TileDesc {
+  int64_t src;     // input byte offset of the tile (relative to d_in)
+  int64_t dst;     // output byte offset of the tile (relative to d_out)
+  int64_t rel;     // input offset of the tile within its message
+  int32_t len;     // input bytes of the tile (> 0; decode: multiple of 4)
+  int32_t msg;     // message index (batched), 0 otherwise
+  int32_t flags;   // kFlagFinal
+  int32_t ntiles;  // tiles of the message (batched)
+};
+static_assert(sizeof(TileDesc) == 40, "TileDesc layout");
+
+// ------------------------------------------------------- alphabet (GPU) ---
+// Table II: 6-bit value -> ASCII by range offsets.
+__device__ __forceinline__ uint32_t ascii_of(uint32_t v) {
+  int off = v < 26 ? 65 : v < 52 ? 71 : v < 62 ? -4 : v == 62 ? -19 : -16;
+  return static_cast<uint32_t>(static_cast<int>(v) + off);
+}
+
+// ---------------------------------------------------- smem word access ---
+// Load N little-endian words of the stream starting at smem byte address p.
+// ALIGN: guaranteed alignment of p (16, 4 or 1); ALIGN 1 realigns with
+// funnel shifts (the byte shift is warp-uniform).
+template <int ALIGN, int N>
+__device__ __forceinline__ void load_words(const uint8_t *p, uint32_t (&w)[N]) {
+  if constexpr (ALIGN == 16 && N == 4) {
+    const uint4 v = *reinterpret_cast<const uint4 *>(p);
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  } else if constexpr (ALIGN >= 4) {
+    const uint32_t *q = reinterpret_cast<const uint32_t *>(p);
+#pragma unroll
+    for (int k = 0; k < N; ++k) w[k] = q[k];
+  } else {
+    const uint32_t r = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) & 3);
+    const uint32_t *q = reinterpret_cast<const uint32_t *>(p - r);
+    uint32_t x[N + 1];
+#pragma unroll
+    for (int k = 0; k <= N; ++k) x[k] = q[k];
+#pragma unroll
+    for (int k = 0; k < N; ++k) w[k] = __funnelshift_r(x[k], x[k + 1], 8 * r);
+  }
+}
+
+// Store N words D (stream bytes [X, X+4N)) to smem byte address p = base+X.
+// Lanes of a warp hold consecutive, adjacent 4N-byte runs; `active` lanes
+// form a prefix of the warp.  ALIGN 1: each lane writes the aligned words it
+// owns completely plus the word it shares with the next lane (built from the
+// next lane's first word via a shuffle); the words shared with the previous /
+// next warp are written byte by byte.  Must be called by all 32 lanes.
+template <int ALIGN, int N>
+__device__ __forceinline__ void store_words(uint8_t *p, const uint32_t (&D)[N], bool active,
+                                            int lane) {
+  if constexpr (ALIGN == 16 && N == 4) {
+    if (active) *reinterpret_cast<uint4 *>(p) = make_uint4(D[0], D[1], D[2], D[3]);
+  } else if constexpr (ALIGN >= 4) {
+    if (active) {
+      uint32_t *q = reinterpret_cast<uint32_t *>(p);
+#pragma unroll
+      for (int k = 0; k < N; ++k) q[k] = D[k];
+    }
+  } else {
+    const uint32_t r = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) & 3);
+    const uint32_t nxt = __shfl_down_sync(0xffffffffu, D[0], 1);
+    const bool nxt_active = __shfl_down_sync(0xffffffffu, active ? 1u : 0u, 1) != 0 && lane < 31;
+    if (!active) return;
+    if (r == 0) {
+      uint32_t *q = reinterpret_cast<uint32_t *>(p);
+#pragma unroll
+      for (int k = 0; k < N; ++k) q[k] = D[k];
+      return;
+    }
+    const uint32_t s = 8 * r;
+    uint32_t *q = reinterpret_cast<uint32_t *>(p - r);
+#pragma unroll
+    for (int k = 1; k < N; ++k) q[k] = __funnelshift_l(D[k - 1], D[k], s);
+    if (nxt_active) {
+      q[N] = __funnelshift_l(D[N - 1], nxt, s);
+    } else {
+      uint8_t *b = reinterpret_cast<uint8_t *>(q + N);
+      for (uint32_t i = 0; i < r; ++i) b[i] = static_cast<uint8_t>(D[N - 1] >> (8 * (4 - r + i)));
+    }
+    if (lane == 0) {
+      for (uint32_t i = 0; i < 4 - r; ++i) p[i] = static_cast<uint8_t>(D[0] >> (8 * i));
+    }
+  }
+}
+
+// ------------------------------------------------------------- encode ---
+// One group (Alg 1 main loop body): x holds s_i<<16 | s_{i+1}<<8 |
+// s_{i+2} in its low 24 bits; TOPZERO says whether bits 24..31 are zero.
+// The four 6-bit fields are s_i/4, (s_i*16 mod 64) + s_{i+1}/16,
+// (s_{i+1}*4 mod 64) + s_{i+2}/64 and s_{i+2} mod 64, i.e. bits 23..18,
+// 17..12, 11..6, 5..0 of x; each is mapped through the 64-entry smem table B
+// and the four characters are packed little-endian (first char = byte 0).
+template <bool TOPZERO>
+__device__ __forceinline__ uint32_t enc_group(uint32_t x, const uint8_t *tab) {
+  const uint32_t i0 = TOPZERO ? (x >> 18) : ((x >> 18) & 63u);
+  const uint32_t i1 = (x >> 12) & 63u;
+  const uint32_t i2 = (x >> 6) & 63u;
+  const uint32_t i3 = x & 63u;
+  const uint32_t c0 = tab[i0], c1 = tab[i1], c2 = tab[i2], c3 = tab[i3];
+  return __byte_perm(__byte_perm(c0, c1, 0x3340), __byte_perm(c2, c3, 0x3340), 0x5410);
+}
+
+// 12 input bytes (w0..w2, little-endian) -> 16 output chars (c0..c3).
+// __byte_perm reorders each 3-byte group big-endian (the GPU counterpart of
+// the paper's vpshufb step in enc_reshuffle).
+__device__ __forceinline__ void encode12(const uint32_t (&w)[3], uint32_t (&c)[4],
+                                         const uint8_t *tab) {
+  c[0] = enc_group<true>(__byte_perm(w[0], 0u, 0x4012), tab);    // b0 b1 b2
+  c[1] = enc_group<false>(__byte_perm(w[0], w[1], 0x3345), tab);  // b3 b4 b5
+  c[2] = enc_group<false>(__byte_perm(w[1], w[2], 0x2234), tab);  // b6 b7 b8
+  c[3] = enc_group<true>(__byte_perm(w[2], 0u, 0x4123), tab);    // b9 b10 b11
+}
+
+// Replace byte i (0..15) of the 4-word vector with value v.
+__device__ __forceinline__ void set_byte16(uint32_t (&c)[4], int i, uint32_t v) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (4 * k + b == i) c[k] = (c[k] & ~(0xFFu << (8 * b))) | (v << (8 * b));
+    }
+  }
+}
+
+// Encode one tile: L input bytes at sin -> 4*ceil(L/3) chars at sout.
+// Alg 1's tail is handled by the one thread whose 12-byte run
+// crosses L: missing bytes are zero (so the emitted fields equal
+// (s_i*16) mod 64 and (s_{i+1}*4) mod 64) and '=' pads are substituted.
+template <int IA, int OA>
+__device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *sout,
+                                            const uint8_t *tab, int tid, int lane) {
+#pragma unroll
+  for (int pass = 0; pass < kEncPasses; ++pass) {
+    const int bo = pass * (kNT * 12) + tid * 12;
+    const int co = pass * (kNT * 16) + tid * 16;
+    const bool active = bo < L;
+    if (!__any_sync(0xffffffffu, active)) break;
+    uint32_t w[3];
+    load_words<(IA >= 4 ? 4 : 1), 3>(sin + bo, w);
+    const int rem = L - bo;
+    const bool partial = active && rem < 12;
+    if (partial) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int keep = rem - 4 * k;
+        if (keep <= 0) w[k] = 0;
+        else if (keep < 4) w[k] &= (1u << (8 * keep)) - 1u;
+      }
+    }
+    uint32_t c[4];
+    encode12(w, c, tab);
+    if (partial) {
+      const int left = rem % 3;           // 1 -> "xx==", 2 -> "xxx="
+      if (left != 0) {
+        const int last = 4 * (rem / 3);   // first char of the partial group
+        set_byte16(c, last + 3, '=');
+        if (left == 1) set_byte16(c, last + 2, '=');
+      }
+    }
+    store_words<OA, 4>(sout + co, c, active, lane);
+  }
+}
+
+// ------------------------------------------------------------- decode ---
+// Decode one tile: L chars (multiple of 4) at sin -> 3*L/4 bytes at sout.
+// Table lookups classify and translate (A of Alg 2; validity rule of
+// P:952-958); the four 6-bit values of a quad are packed as
+// a<<18 | b<<12 | c<<6 | d (bit layout P:1013-1030) and three
+// __byte_perm write the 12 output bytes of 4 quads.  Errors take the slow
+// path only when some lane of the warp saw an invalid byte (__any_sync):
+// per-char mask, final-quad '=' rules (reading R-pad), first bad offset,
+// warp __reduce_min_sync.  Returns (lane 0 meaningful) the tile-relative
+// minimum error offset, or 0xFFFFFFFF.
+template <int IA, int OA>
+__device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8_t *sout,
+                                                const uint8_t *tab, int tid, int lane,
+                                                bool final_tile, uint32_t ch2, uint32_t ch1) {
+  uint32_t errmin = 0xFFFFFFFFu;
+#pragma unroll
+  for (int pass = 0; pass < kDecPasses; ++pass) {
+    const int co = pass * (kNT * 16) + tid * 16;
+    const int bo = pass * (kNT * 12) + tid * 12;
+    const bool active = co < L;
+    if (!__any_sync(0xffffffffu, active)) break;
+    uint32_t w[4];
+    load_words<IA, 4>(sin + co, w);
+    const int rem = L - co;
+    if (!active || rem < 16) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (!active || 4 * k >= rem) w[k] = 0x41414141u;  // "AAAA": ignored filler
+    }
+    uint32_t v[16];
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[4 * k + 0] = tab[w[k] & 0xFFu];
+      v[4 * k + 1] = tab[__byte_perm(w[k], 0u, 0x4441)];
+      v[4 * k + 2] = tab[__byte_perm(w[k], 0u, 0x4442)];
+      v[4 * k + 3] = tab[w[k] >> 24];
+      acc |= v[4 * k + 0] | v[4 * k + 1];
+      acc |= v[4 * k + 2] | v[4 * k + 3];
+    }
+    const bool bad = (acc & 0x80u) != 0;
+    if (__any_sync(0xffffffffu, bad)) {
+      uint32_t pos = 0xFFFFFFFFu;
+      if (bad) {
+        uint32_t mask = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mask |= ((v[j] >> 7) & 1u) << j;
+        // Final quad of the stream (reading R-pad): '=' allowed at m-2 and
+        // m-1, and '=' at m-2 forces '=' at m-1; '=' contributes value 0.
+        if (final_tile && co + 16 >= L && co < L) {
+          const int j1 = L - 1 - co, j2 = L - 2 - co;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j == j2 && ch2 == '=') { mask &= ~(1u << j); v[j] = 0; }
+            if (j == j1) {
+              if (ch1 == '=') { mask &= ~(1u << j); v[j] = 0; }
+              else if (ch2 == '=') mask |= 1u << j;
+            }
+          }
+        }
+        if (mask) pos = static_cast<uint32_t>(co) + __ffs(mask) - 1;
+      }
+      const uint32_t wmin = __reduce_min_sync(0xffffffffu, pos);
+      errmin = min(errmin, wmin);
+    }
+    uint32_t V[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      V[k] = ((v[4 * k] * 64u + v[4 * k + 1]) * 64u + v[4 * k + 2]) * 64u + v[4 * k + 3];
+    uint32_t o[3];
+    o[0] = __byte_perm(V[0], V[1], 0x6012);
+    o[1] = __byte_perm(V[1], V[2], 0x5601);
+    o[2] = __byte_perm(V[2], V[3], 0x4560);
+    store_words<(OA >= 4 ? 4 : 1), 3>(sout + bo, o, active, lane);
+  }
+  return errmin;
+}
+
+}  // namespace b64

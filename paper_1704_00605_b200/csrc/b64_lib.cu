@@ -1,0 +1,838 @@
+// b64_lib.cu -- sm_100a kernels and the C ABI of libb64gpu.so (include/b64gpu.h).
+//
+// Kernel structure:
+//   persistent grid (2 CTAs per SM); per CTA 8 compute warps + 1 producer
+//   warp.  The producer lane streams input tiles HBM -> smem with 1-D bulk
+//   (TMA) copies into a 4-stage mbarrier ring; compute warps transform the
+//   tile smem -> smem; one elected thread writes the output tile smem -> HBM
+//   with a bulk copy (plus byte stores for the <16-byte unaligned edges).
+//   Every HBM access is thus a 16-byte-granular bulk transfer, although
+//   3-byte groups and 4-char quads do not align to 16 B.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "../../include/b64gpu.h"
+#include "b64_codec.cuh"
+#include "b64_ptx.cuh"
+
+namespace b64 {
+
+using namespace ptx;
+
+// ------------------------------------------------------------ smem ---
+template <int IN_BYTES, int OUT_BYTES>
+struct alignas(128) Smem {
+  static constexpr int kInStride = round_up_c(IN_BYTES + 32, 128);
+  static constexpr int kOutStride = round_up_c(OUT_BYTES + 32, 128);
+  uint8_t in[kStagesIn][kInStride];
+  uint8_t out[kStagesOut][kOutStride];
+  TileDesc desc[kStagesIn];
+  uint64_t full[kStagesIn];
+  uint64_t empty[kStagesIn];
+  alignas(16) uint8_t table[256];
+};
+using EncSmem = Smem<kEncIn, kEncOut>;
+using DecSmem = Smem<kDecIn, kDecOut>;
+
+struct DecWs {                 // per-(device, stream) decode scratch (self-resetting)
+  unsigned long long errkey;   // min error offset, ~0 = none
+  unsigned int done;           // CTAs finished
+  unsigned int pad;
+};
+
+// ------------------------------------------------- tile descriptors ---
+__device__ __forceinline__ TileDesc enc_single_desc(int64_t j, int64_t n) {
+  TileDesc d;
+  d.src = j * kEncIn;
+  d.dst = j * kEncOut;
+  d.rel = d.src;
+  const int64_t left = n - d.src;
+  d.len = static_cast<int32_t>(left < kEncIn ? left : kEncIn);
+  d.msg = 0;
+  d.flags = 0;
+  d.ntiles = 0;
+  return d;
+}
+
+__device__ __forceinline__ TileDesc dec_single_desc(int64_t j, int64_t ntiles, int64_t chars,
+                                                    bool final_pad_rules) {
+  TileDesc d;
+  d.src = j * kDecIn;
+  d.dst = j * kDecOut;
+  d.rel = d.src;
+  const int64_t left = chars - d.src;
+  d.len = static_cast<int32_t>(left < kDecIn ? left : kDecIn);
+  d.msg = 0;
+  d.flags = (final_pad_rules && j == ntiles - 1) ? kFlagFinal : 0;
+  d.ntiles = 0;
+  return d;
+}
+
+// --------------------------------------------------- producer warp ---
+// Lane 0 owns the ring: wait for the slot, publish the descriptor, arm the
+// full barrier with the byte count and issue the bulk copy of the tile's
+// 16-byte aligned window.  Batched descriptors are fetched 32 at a time by
+// the whole warp and handed to lane 0 by shuffles.
+template <bool BATCH, bool DECODE, class SmemT>
+__device__ __forceinline__ void producer_loop(SmemT &S, const uint8_t *in, int64_t ntiles,
+                                              int64_t n_or_chars, bool final_pad_rules,
+                                              const TileDesc *descs, int lane) {
+  const uint64_t pol = policy_evict_first();
+  int it = 0;
+  TileDesc mine;
+  for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
+    TileDesc d;
+    if constexpr (BATCH) {
+      if ((it & 31) == 0) {
+        const int64_t jj = j + static_cast<int64_t>(lane) * gridDim.x;
+        if (jj < ntiles) mine = descs[jj];
+      }
+      const int src_lane = it & 31;
+      d.src = __shfl_sync(0xffffffffu, mine.src, src_lane);
+      d.dst = __shfl_sync(0xffffffffu, mine.dst, src_lane);
+      d.rel = __shfl_sync(0xffffffffu, mine.rel, src_lane);
+      d.len = __shfl_sync(0xffffffffu, mine.len, src_lane);
+      d.msg = __shfl_sync(0xffffffffu, mine.msg, src_lane);
+      d.flags = __shfl_sync(0xffffffffu, mine.flags, src_lane);
+      d.ntiles = __shfl_sync(0xffffffffu, mine.ntiles, src_lane);
+    } else {
+      if constexpr (DECODE) {
+        d = dec_single_desc(j, ntiles, n_or_chars, final_pad_rules);
+      } else {
+        d = enc_single_desc(j, n_or_chars);
+      }
+    }
+    if (lane == 0) {
+      const int s = it % kStagesIn;
+      if (it >= kStagesIn) mbar_wait(&S.empty[s], ((it / kStagesIn) & 1) ^ 1);
+      S.desc[s] = d;
+      const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
+      const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
+      const uintptr_t g1 = (g + static_cast<uintptr_t>(d.len) + 15) & ~static_cast<uintptr_t>(15);
+      const uint32_t bytes = static_cast<uint32_t>(g1 - g0);
+      mbar_arrive_expect_tx(&S.full[s], bytes);
+      bulk_g2s(S.in[s], reinterpret_cast<const void *>(g0), bytes, &S.full[s], pol);
+    }
+  }
+}
+
+// Write `len` bytes staged at sbuf (data byte j at sbuf[j]; sbuf has the same
+// address mod 16 as gdst) to gdst: aligned interior by one bulk copy, the
+// unaligned head/tail (< 16 B each) by byte stores of warp 0.
+__device__ __forceinline__ void copy_out(uint8_t *gdst, const uint8_t *sbuf, int len, int tid,
+                                         uint64_t pol) {
+  const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
+  const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
+  const uintptr_t a1 = (g + static_cast<uintptr_t>(len)) & ~static_cast<uintptr_t>(15);
+  if (a1 > a0) {
+    if (tid == 0) {
+      bulk_s2g(reinterpret_cast<void *>(a0), sbuf + (a0 - g), static_cast<uint32_t>(a1 - a0), pol);
+      bulk_commit();
+    }
+    const int head = static_cast<int>(a0 - g);
+    const int tail = static_cast<int>(g + len - a1);
+    if (tid < head) {
+      gdst[tid] = sbuf[tid];
+    } else if (tid >= 16 && tid < 16 + tail) {
+      const int j = static_cast<int>(a1 - g) + (tid - 16);
+      gdst[j] = sbuf[j];
+    }
+  } else {
+    for (int j = tid; j < len; j += kNT) gdst[j] = sbuf[j];
+  }
+}
+
+// ------------------------------------------------------ encode kernel ---
+template <int IA, int OA, bool BATCH>
+__global__ void __launch_bounds__(kThreads, 2)
+    encode_kernel(const uint8_t *__restrict__ in, int64_t n, uint8_t *__restrict__ out,
+                  int64_t ntiles_arg, const TileDesc *__restrict__ descs,
+                  const int64_t *__restrict__ ntiles_dev) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  EncSmem &S = *reinterpret_cast<EncSmem *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = BATCH ? *ntiles_dev : ntiles_arg;
+
+  if (tid < 64) S.table[tid] = static_cast<uint8_t>(ascii_of(tid));  // Table I / II
+  if (tid == 0) {
+    for (int s = 0; s < kStagesIn; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], kWarpsC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kWarpsC) {
+    producer_loop<BATCH, false>(S, in, ntiles, n, false, descs, lane);
+    return;
+  }
+
+  const uint64_t pol_out = policy_evict_normal();
+  int it = 0;
+  for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
+    const int s = it % kStagesIn, so = it % kStagesOut;
+    mbar_wait(&S.full[s], (it / kStagesIn) & 1);
+    const TileDesc d = S.desc[s];
+    const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
+    uint8_t *gdst = out + d.dst;
+    const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
+    encode_tile<IA, OA>(S.in[s] + imis, d.len, S.out[so] + omis, S.table, tid, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[s]);
+    fence_proxy_async_smem();
+    if (tid == 0) bulk_wait_read<kStagesOut - 2>();  // staging slot of tile it+1 is free
+    named_bar_sync(1, kNT);
+    const int olen = 4 * ((d.len + 2) / 3);
+    copy_out(gdst, S.out[so] + omis, olen, tid, pol_out);
+  }
+  if (tid == 0) bulk_wait<0>();
+}
+
+// ------------------------------------------------------ decode kernel ---
+// Final result of a whole-stream decode (single buffer / shard).
+__device__ void finalize_single(const uint8_t *in, int64_t m, bool final_shard,
+                                unsigned long long errkey, b64_result *res) {
+  const int64_t q = m / 4, r = m % 4;
+  int32_t p = 0;
+  if (final_shard && r == 0 && q > 0 && in[m - 1] == '=') p = (in[m - 2] == '=') ? 2 : 1;
+  int64_t err = errkey == ~0ull ? -1 : static_cast<int64_t>(errkey);
+  int32_t st;
+  int64_t olen;
+  if (err < 0 && r != 0) err = 4 * q;
+  if (err < 0) {
+    st = B64_OK;
+    olen = 3 * q - p;
+  } else if (r != 0 && err == 4 * q) {
+    st = B64_ERR_LENGTH;
+    olen = 3 * q;
+    p = 0;
+  } else {
+    st = B64_ERR_INVALID_CHAR;
+    olen = 3 * (err / 4);
+    p = 0;
+  }
+  res->out_len = olen;
+  res->err_pos = err;
+  res->status = st;
+  res->pad_count = p;
+}
+
+template <int IA, int OA, bool BATCH>
+__global__ void __launch_bounds__(kThreads, 2)
+    decode_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
+                  int64_t ntiles_arg, int final_shard, DecWs *ws, b64_result *res,
+                  const TileDesc *__restrict__ descs, const int64_t *__restrict__ ntiles_dev,
+                  const int64_t *__restrict__ in_off, const int64_t *__restrict__ out_off,
+                  int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
+                  int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  DecSmem &S = *reinterpret_cast<DecSmem *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = BATCH ? *ntiles_dev : ntiles_arg;
+  const int64_t chars = BATCH ? 0 : 4 * (m / 4);
+  const bool pad_rules = final_shard != 0 && (m % 4) == 0;
+
+  // Inverse map A: invalid everywhere, then A(B(v)) = v.
+  if (tid < 256) S.table[tid] = kInvalid;
+  if (tid == 0) {
+    for (int s = 0; s < kStagesIn; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], kWarpsC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid < 64) S.table[ascii_of(tid)] = static_cast<uint8_t>(tid);
+  __syncthreads();
+
+  if (warp == kWarpsC) {
+    producer_loop<BATCH, true>(S, in, ntiles, chars, pad_rules, descs, lane);
+    return;
+  }
+
+  const uint64_t pol_out = policy_evict_normal();
+  int it = 0;
+  for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
+    const int s = it % kStagesIn, so = it % kStagesOut;
+    mbar_wait(&S.full[s], (it / kStagesIn) & 1);
+    const TileDesc d = S.desc[s];
+    const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
+    uint8_t *gdst = out + d.dst;
+    const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
+    const uint8_t *sin = S.in[s] + imis;
+    const bool fin = (d.flags & kFlagFinal) != 0;
+    uint32_t ch1 = 0, ch2 = 0;
+    int pads = 0;
+    if (fin) {
+      ch1 = sin[d.len - 1];
+      ch2 = sin[d.len - 2];
+      pads = ch1 == '=' ? (ch2 == '=' ? 2 : 1) : 0;
+    }
+    const uint32_t werr =
+        decode_tile<IA, OA>(sin, d.len, S.out[so] + omis, S.table, tid, lane, fin, ch2, ch1);
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&S.empty[s]);
+      if (werr != 0xFFFFFFFFu) {
+        // First-error reduction: one 64-bit atomicMin per warp,
+        // skipped when a smaller offset is already recorded.
+        const unsigned long long pos = static_cast<unsigned long long>(d.rel) + werr;
+        unsigned long long *tgt =
+            BATCH ? reinterpret_cast<unsigned long long *>(err_pos + d.msg) : &ws->errkey;
+        if (pos < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, pos);
+        __threadfence();
+      }
+    }
+    fence_proxy_async_smem();
+    if (tid == 0) bulk_wait_read<kStagesOut - 2>();
+    named_bar_sync(1, kNT);
+    const int olen = 3 * (d.len / 4) - pads;
+    copy_out(gdst, S.out[so] + omis, olen, tid, pol_out);
+    if constexpr (BATCH) {
+      // Per-message completion: the CTA finishing the message's last tile
+      // writes its result (status is a pure function of err_pos).
+      if (tid == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(msg_done + d.msg, 1u);
+        if (prev == static_cast<unsigned>(d.ntiles - 1)) {
+          __threadfence();
+          const int64_t i = d.msg;
+          const int64_t len = in_off[i + 1] - in_off[i];
+          const int64_t q = len / 4, r = len % 4;
+          const int64_t cap = out_off[i + 1] - out_off[i];
+          const unsigned long long e =
+              atomicOr(reinterpret_cast<unsigned long long *>(err_pos + i), 0ull);
+          int64_t err = e == static_cast<unsigned long long>(LLONG_MAX) ? -1
+                                                                         : static_cast<int64_t>(e);
+          if (err < 0 && r != 0) err = 4 * q;
+          if (err < 0) {
+            status[i] = B64_OK;
+            out_len[i] = cap;
+          } else if (r != 0 && err == 4 * q) {
+            status[i] = B64_ERR_LENGTH;
+            out_len[i] = 3 * q;
+          } else {
+            status[i] = B64_ERR_INVALID_CHAR;
+            out_len[i] = 3 * (err / 4);
+          }
+          err_pos[i] = err;
+        }
+      }
+    }
+  }
+  if (tid == 0) bulk_wait<0>();
+
+  if constexpr (!BATCH) {
+    // Last CTA out computes the result record and resets the scratch.
+    if (tid == 0) {
+      __threadfence();
+      const unsigned prev = atomicAdd(&ws->done, 1u);
+      if (prev == gridDim.x - 1) {
+        __threadfence();
+        const unsigned long long e = atomicOr(&ws->errkey, 0ull);
+        finalize_single(in, m, final_shard != 0, e, res);
+        ws->errkey = ~0ull;
+        ws->done = 0;
+        __threadfence_system();
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------ batch planner ---
+// One CTA: exclusive scans of per-message output sizes and tile counts,
+// then the tile descriptors (messages -> tiles by prefix-summed lengths).
+constexpr int kPlanThreads = 1024;
+constexpr int kPlanItems = 8;
+
+struct PlanHeader {
+  int64_t ntiles;
+  int64_t capacity;  // descriptors that fit in the workspace
+  int64_t overflow;  // 1 if capacity was exceeded (nothing is processed)
+  int64_t pad;
+};
+
+__device__ __forceinline__ void block_exclusive_scan2(int64_t a, int64_t b, int64_t &pa,
+                                                      int64_t &pb, int64_t &ta, int64_t &tb,
+                                                      int64_t *sh /* 2*32 + 2 */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t xa = __shfl_up_sync(0xffffffffu, ia, o);
+    const int64_t xb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) {
+      ia += xa;
+      ib += xb;
+    }
+  }
+  if (lane == 31) {
+    sh[warp] = ia;
+    sh[32 + warp] = ib;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int64_t wa = sh[lane], wb = sh[32 + lane];
+    int64_t sa = wa, sb = wb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t xa = __shfl_up_sync(0xffffffffu, sa, o);
+      const int64_t xb = __shfl_up_sync(0xffffffffu, sb, o);
+      if (lane >= o) {
+        sa += xa;
+        sb += xb;
+      }
+    }
+    sh[lane] = sa - wa;  // exclusive warp prefix
+    sh[32 + lane] = sb - wb;
+    if (lane == 31) {
+      sh[64] = sa;
+      sh[65] = sb;
+    }
+  }
+  __syncthreads();
+  pa = sh[warp] + ia - a;
+  pb = sh[32 + warp] + ib - b;
+  ta = sh[64];
+  tb = sh[65];
+  __syncthreads();
+}
+
+template <bool DECODE>
+__global__ void __launch_bounds__(kPlanThreads)
+    plan_kernel(const uint8_t *__restrict__ in, const int64_t *__restrict__ in_off, int64_t k,
+                int64_t *__restrict__ out_off, PlanHeader *hdr, TileDesc *__restrict__ descs,
+                int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
+                int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
+  __shared__ int64_t sh[66];
+  const int64_t cap = hdr->capacity;
+  constexpr int TILE = DECODE ? kDecIn : kEncIn;
+  int64_t carry_out = 0, carry_tiles = 0;
+  for (int64_t base = 0; base < k; base += static_cast<int64_t>(kPlanThreads) * kPlanItems) {
+    const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * kPlanItems;
+    int64_t len[kPlanItems], osz[kPlanItems];
+    int32_t nt[kPlanItems];
+    int64_t sum_o = 0, sum_t = 0;
+#pragma unroll
+    for (int t = 0; t < kPlanItems; ++t) {
+      const int64_t i = i0 + t;
+      len[t] = 0;
+      osz[t] = 0;
+      nt[t] = 0;
+      if (i < k) {
+        const int64_t a = in_off[i], b = in_off[i + 1];
+        len[t] = b - a;
+        if (DECODE) {
+          const int64_t q = len[t] / 4;
+          int64_t p = 0;
+          if (len[t] % 4 == 0 && q > 0 && in[b - 1] == '=') p = (in[b - 2] == '=') ? 2 : 1;
+          osz[t] = 3 * q - p;
+          nt[t] = static_cast<int32_t>((4 * q + TILE - 1) / TILE);
+        } else {
+          osz[t] = 4 * ((len[t] + 2) / 3);
+          nt[t] = static_cast<int32_t>((len[t] + TILE - 1) / TILE);
+        }
+      }
+      sum_o += osz[t];
+      sum_t += nt[t];
+    }
+    int64_t po, pt, to, tt;
+    block_exclusive_scan2(sum_o, sum_t, po, pt, to, tt, sh);
+    int64_t run_o = carry_out + po, run_t = carry_tiles + pt;
+#pragma unroll
+    for (int t = 0; t < kPlanItems; ++t) {
+      const int64_t i = i0 + t;
+      if (i < k) {
+        out_off[i] = run_o;
+        const int64_t src0 = in_off[i];
+        if (DECODE) {
+          msg_done[i] = 0;
+          const int64_t q = len[t] / 4, r = len[t] % 4;
+          if (nt[t] == 0) {  // no complete quad: decided here
+            if (r == 0) {
+              status[i] = B64_OK;
+              err_pos[i] = -1;
+            } else {
+              status[i] = B64_ERR_LENGTH;
+              err_pos[i] = 0;
+            }
+            out_len[i] = 0;
+          } else {
+            err_pos[i] = LLONG_MAX;
+          }
+          for (int32_t u = 0; u < nt[t]; ++u) {
+            const int64_t tix = run_t + u;
+            if (tix < cap) {
+              TileDesc d;
+              d.rel = static_cast<int64_t>(u) * TILE;
+              d.src = src0 + d.rel;
+              d.dst = run_o + static_cast<int64_t>(u) * (TILE / 4 * 3);
+              const int64_t left = 4 * q - d.rel;
+              d.len = static_cast<int32_t>(left < TILE ? left : TILE);
+              d.msg = static_cast<int32_t>(i);
+              d.flags = (u == nt[t] - 1 && r == 0) ? kFlagFinal : 0;
+              d.ntiles = nt[t];
+              descs[tix] = d;
+            }
+          }
+        } else {
+          for (int32_t u = 0; u < nt[t]; ++u) {
+            const int64_t tix = run_t + u;
+            if (tix < cap) {
+              TileDesc d;
+              d.rel = static_cast<int64_t>(u) * TILE;
+              d.src = src0 + d.rel;
+              d.dst = run_o + static_cast<int64_t>(u) * (TILE / 3 * 4);
+              const int64_t left = len[t] - d.rel;
+              d.len = static_cast<int32_t>(left < TILE ? left : TILE);
+              d.msg = static_cast<int32_t>(i);
+              d.flags = 0;
+              d.ntiles = nt[t];
+              descs[tix] = d;
+            }
+          }
+        }
+      }
+      run_o += osz[t];
+      run_t += nt[t];
+    }
+    carry_out += to;
+    carry_tiles += tt;
+  }
+  if (threadIdx.x == 0) {
+    out_off[k] = carry_out;
+    const bool ovf = carry_tiles > cap;
+    hdr->overflow = ovf ? 1 : 0;
+    hdr->ntiles = ovf ? 0 : carry_tiles;
+  }
+}
+
+}  // namespace b64
+
+// =====================================================================
+// Host side
+// =====================================================================
+namespace {
+
+using namespace b64;
+
+struct DevInfo {
+  int sms = 0;
+  bool attrs_set = false;
+};
+
+std::mutex g_mu;
+std::map<int, DevInfo> g_dev;
+
+struct StreamWs {
+  DecWs *d_ws = nullptr;
+  b64_result *h_res = nullptr;  // mapped pinned
+  b64_result *d_res = nullptr;  // device alias of h_res
+};
+std::map<std::pair<int, uintptr_t>, StreamWs> g_ws;
+
+int ctas_per_sm() { return 2; }
+
+template <class K>
+cudaError_t set_smem(K kernel, int bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// Kernel tables indexed by alignment class (0: 16-aligned, 1: 4-aligned, 2: unaligned).
+using EncFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, const TileDesc *,
+                       const int64_t *);
+using DecFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int, DecWs *, b64_result *,
+                       const TileDesc *, const int64_t *, const int64_t *, const int64_t *,
+                       int64_t *, int64_t *, int32_t *, unsigned int *);
+
+EncFn enc_table[3][3] = {
+    {encode_kernel<16, 16, false>, encode_kernel<16, 4, false>, encode_kernel<16, 1, false>},
+    {encode_kernel<4, 16, false>, encode_kernel<4, 4, false>, encode_kernel<4, 1, false>},
+    {encode_kernel<1, 16, false>, encode_kernel<1, 4, false>, encode_kernel<1, 1, false>},
+};
+DecFn dec_table[3][3] = {
+    {decode_kernel<16, 16, false>, decode_kernel<16, 4, false>, decode_kernel<16, 1, false>},
+    {decode_kernel<4, 16, false>, decode_kernel<4, 4, false>, decode_kernel<4, 1, false>},
+    {decode_kernel<1, 16, false>, decode_kernel<1, 4, false>, decode_kernel<1, 1, false>},
+};
+
+int align_class(const void *p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  return (a & 15) == 0 ? 0 : (a & 3) == 0 ? 1 : 2;
+}
+
+// Device info + one-time kernel attributes.
+bool device_setup(int *dev_out, int *sms_out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevInfo &di = g_dev[dev];
+  if (!di.attrs_set) {
+    if (cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return false;
+    for (auto &row : enc_table)
+      for (auto f : row)
+        if (set_smem(f, sizeof(EncSmem)) != cudaSuccess) return false;
+    for (auto &row : dec_table)
+      for (auto f : row)
+        if (set_smem(f, sizeof(DecSmem)) != cudaSuccess) return false;
+    if (set_smem(encode_kernel<1, 1, true>, sizeof(EncSmem)) != cudaSuccess) return false;
+    if (set_smem(decode_kernel<1, 1, true>, sizeof(DecSmem)) != cudaSuccess) return false;
+    di.attrs_set = true;
+  }
+  *dev_out = dev;
+  *sms_out = di.sms;
+  return true;
+}
+
+StreamWs *stream_ws(int dev, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, reinterpret_cast<uintptr_t>(stream));
+  auto it = g_ws.find(key);
+  if (it != g_ws.end()) return &it->second;
+  StreamWs w;
+  if (cudaMalloc(&w.d_ws, sizeof(DecWs)) != cudaSuccess) return nullptr;
+  DecWs init{~0ull, 0u, 0u};
+  if (cudaMemcpy(w.d_ws, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  if (cudaHostAlloc(&w.h_res, sizeof(b64_result), cudaHostAllocMapped) != cudaSuccess) return nullptr;
+  if (cudaHostGetDevicePointer(&w.d_res, w.h_res, 0) != cudaSuccess) return nullptr;
+  auto res = g_ws.emplace(key, w);
+  return &res.first->second;
+}
+
+int64_t grid_for(int64_t ntiles, int sms) {
+  int64_t g = static_cast<int64_t>(sms) * ctas_per_sm();
+  if (ntiles < g) g = ntiles;
+  return g < 1 ? 1 : g;
+}
+
+int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
+                  b64_result *d_result, cudaStream_t stream, DecWs *ws) {
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  const int64_t chars = 4 * (m / 4);
+  const int64_t ntiles = (chars + kDecIn - 1) / kDecIn;
+  const int64_t grid = grid_for(ntiles, sms);
+  DecFn f = dec_table[align_class(d_in)][align_class(d_out)];
+  f<<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem), stream>>>(
+      d_in, m, d_out, ntiles, final_shard, ws, d_result, nullptr, nullptr, nullptr, nullptr,
+      nullptr, nullptr, nullptr, nullptr);
+  return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
+}
+
+size_t ws_layout(int64_t k, int64_t total_in, int direction, size_t *off_descs, size_t *off_done,
+                 int64_t *cap) {
+  const int64_t tile = direction ? kDecIn : kEncIn;
+  const int64_t c = (total_in > 0 ? total_in / tile : 0) + k + 1;
+  size_t o = 256;  // PlanHeader
+  *off_descs = o;
+  o += static_cast<size_t>(c) * sizeof(TileDesc);
+  o = (o + 255) & ~static_cast<size_t>(255);
+  *off_done = o;
+  o += static_cast<size_t>(k > 0 ? k : 1) * sizeof(unsigned int);
+  o = (o + 255) & ~static_cast<size_t>(255);
+  *cap = c;
+  return o;
+}
+
+}  // namespace
+
+// =====================================================================
+// C ABI
+// =====================================================================
+extern "C" {
+
+int64_t b64_encoded_len(int64_t n) { return n < 0 ? -1 : 4 * ((n + 2) / 3); }
+
+int64_t b64_decoded_max_len(int64_t m) { return m < 0 ? -1 : 3 * (m / 4); }
+
+int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t stream) {
+  if (n < 0 || (n > 0 && (d_in == nullptr || d_out == nullptr))) return B64_ERR_ARG;
+  if (n == 0) return 0;
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  const int64_t ntiles = (n + kEncIn - 1) / kEncIn;
+  const int64_t grid = grid_for(ntiles, sms);
+  EncFn f = enc_table[align_class(d_in)][align_class(d_out)];
+  f<<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem), stream>>>(d_in, n, d_out, ntiles,
+                                                                          nullptr, nullptr);
+  if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
+  return 4 * ((n + 2) / 3);
+}
+
+int b64_decode_shard_async(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
+                           b64_result *d_result, b64_stream_t stream) {
+  if (m < 0 || d_result == nullptr || (m >= 4 && (d_in == nullptr || d_out == nullptr)) ||
+      (m > 0 && d_in == nullptr))
+    return B64_ERR_ARG;
+  if (!final_shard && (m % 4) != 0) return B64_ERR_ARG;
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  StreamWs *w = stream_ws(dev, stream);
+  if (w == nullptr) return B64_ERR_CUDA;
+  return decode_launch(d_in, m, final_shard, d_out, d_result, stream, w->d_ws);
+}
+
+int b64_decode_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, b64_result *d_result,
+                     b64_stream_t stream) {
+  return b64_decode_shard_async(d_in, m, 1, d_out, d_result, stream);
+}
+
+int b64_decode(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *out_len,
+               int64_t *err_pos, b64_stream_t stream) {
+  if (m < 0 || (m > 0 && d_in == nullptr) || (m >= 4 && d_out == nullptr)) return B64_ERR_ARG;
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  StreamWs *w = stream_ws(dev, stream);
+  if (w == nullptr) return B64_ERR_CUDA;
+  const int rc = decode_launch(d_in, m, 1, d_out, w->d_res, stream, w->d_ws);
+  if (rc != B64_OK) return rc;
+  if (cudaStreamSynchronize(stream) != cudaSuccess) return B64_ERR_CUDA;
+  b64_result r;
+  std::memcpy(&r, w->h_res, sizeof(r));
+  if (out_len) *out_len = r.out_len;
+  if (err_pos) *err_pos = r.err_pos;
+  return r.status;
+}
+
+size_t b64_batch_workspace_bytes(int64_t k, int64_t total_in, int direction) {
+  if (k < 0 || total_in < 0) return 0;
+  size_t a, b;
+  int64_t cap;
+  return ws_layout(k, total_in, direction ? 1 : 0, &a, &b, &cap);
+}
+
+static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                        uint8_t *d_out, int64_t *d_out_off, int64_t *d_out_len,
+                        int64_t *d_err_pos, int32_t *d_status, void *d_ws, size_t ws_bytes,
+                        cudaStream_t stream, int direction) {
+  if (k < 0 || total_in < 0 || d_in_off == nullptr || d_out_off == nullptr || d_ws == nullptr)
+    return B64_ERR_ARG;
+  if (direction && k > 0 && (d_out_len == nullptr || d_err_pos == nullptr || d_status == nullptr))
+    return B64_ERR_ARG;
+  if (k > INT32_MAX) return B64_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) return B64_ERR_ARG;
+  size_t off_descs, off_done;
+  int64_t cap;
+  const size_t need = ws_layout(k, total_in, direction, &off_descs, &off_done, &cap);
+  if (ws_bytes < need) return B64_ERR_WORKSPACE;
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  uint8_t *ws = static_cast<uint8_t *>(d_ws);
+  PlanHeader *hdr = reinterpret_cast<PlanHeader *>(ws);
+  TileDesc *descs = reinterpret_cast<TileDesc *>(ws + off_descs);
+  unsigned int *done = reinterpret_cast<unsigned int *>(ws + off_done);
+  PlanHeader h{0, cap, 0, 0};
+  if (cudaMemcpyAsync(hdr, &h, sizeof(h), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return B64_ERR_CUDA;
+  if (direction) {
+    plan_kernel<true><<<1, kPlanThreads, 0, stream>>>(d_in, d_in_off, k, d_out_off, hdr, descs,
+                                                       d_err_pos, d_out_len, d_status, done);
+  } else {
+    plan_kernel<false><<<1, kPlanThreads, 0, stream>>>(d_in, d_in_off, k, d_out_off, hdr, descs,
+                                                        nullptr, nullptr, nullptr, done);
+  }
+  if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
+  const int64_t tile = direction ? kDecIn : kEncIn;
+  const int64_t max_tiles = total_in / tile + k;
+  const int64_t grid = grid_for(max_tiles, sms);
+  if (direction) {
+    decode_kernel<1, 1, true><<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem), stream>>>(
+        d_in, 0, d_out, 0, 1, nullptr, nullptr, descs, &hdr->ntiles, d_in_off, d_out_off,
+        d_err_pos, d_out_len, d_status, done);
+  } else {
+    encode_kernel<1, 1, true><<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem), stream>>>(
+        d_in, 0, d_out, 0, descs, &hdr->ntiles);
+  }
+  return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
+}
+
+int b64_encode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                     uint8_t *d_out, int64_t *d_out_off, void *d_ws, size_t ws_bytes,
+                     b64_stream_t stream) {
+  return batch_common(d_in, d_in_off, k, total_in, d_out, d_out_off, nullptr, nullptr, nullptr,
+                      d_ws, ws_bytes, stream, 0);
+}
+
+int b64_decode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                     uint8_t *d_out, int64_t *d_out_off, int64_t *d_out_len, int64_t *d_err_pos,
+                     int32_t *d_status, void *d_ws, size_t ws_bytes, b64_stream_t stream) {
+  return batch_common(d_in, d_in_off, k, total_in, d_out, d_out_off, d_out_len, d_err_pos,
+                      d_status, d_ws, ws_bytes, stream, 1);
+}
+
+int64_t b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, uint8_t *d_scratch_in,
+                        uint8_t *d_scratch_out, b64_stream_t stream) {
+  if (n < 0 || (n > 0 && (!h_in || !h_out || !d_scratch_in || !d_scratch_out))) return B64_ERR_ARG;
+  if (n == 0) return 0;
+  if (cudaMemcpyAsync(d_scratch_in, h_in, n, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return B64_ERR_CUDA;
+  const int64_t ol = b64_encode(d_scratch_in, n, d_scratch_out, stream);
+  if (ol < 0) return ol;
+  if (cudaMemcpyAsync(h_out, d_scratch_out, ol, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+    return B64_ERR_CUDA;
+  if (cudaStreamSynchronize(stream) != cudaSuccess) return B64_ERR_CUDA;
+  return ol;
+}
+
+int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out_len,
+                    int64_t *err_pos, uint8_t *d_scratch_in, uint8_t *d_scratch_out,
+                    b64_stream_t stream) {
+  if (m < 0 || (m > 0 && (!h_in || !d_scratch_in)) || (m >= 4 && (!h_out || !d_scratch_out)))
+    return B64_ERR_ARG;
+  if (m > 0 &&
+      cudaMemcpyAsync(d_scratch_in, h_in, m, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return B64_ERR_CUDA;
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  StreamWs *w = stream_ws(dev, stream);
+  if (w == nullptr) return B64_ERR_CUDA;
+  int rc = decode_launch(d_scratch_in, m, 1, d_scratch_out, w->d_res, stream, w->d_ws);
+  if (rc != B64_OK) return rc;
+  const int64_t cap = 3 * (m / 4);
+  if (cap > 0 &&
+      cudaMemcpyAsync(h_out, d_scratch_out, cap, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+    return B64_ERR_CUDA;
+  if (cudaStreamSynchronize(stream) != cudaSuccess) return B64_ERR_CUDA;
+  b64_result r;
+  std::memcpy(&r, w->h_res, sizeof(r));
+  if (out_len) *out_len = r.out_len;
+  if (err_pos) *err_pos = r.err_pos;
+  return r.status;
+}
+
+int b64_shard(int64_t total, int unit, int world, int rank, int64_t *begin, int64_t *end) {
+  if (total < 0 || unit <= 0 || world <= 0 || rank < 0 || rank >= world || !begin || !end)
+    return B64_ERR_ARG;
+  const __int128 Q = (static_cast<__int128>(total) + unit - 1) / unit;
+  const __int128 g0 = Q * rank / world, g1 = Q * (rank + 1) / world;
+  __int128 b = g0 * unit, e = g1 * unit;
+  if (b > total) b = total;
+  if (e > total) e = total;
+  *begin = static_cast<int64_t>(b);
+  *end = static_cast<int64_t>(e);
+  return B64_OK;
+}
+
+const char *b64_status_str(int status) {
+  switch (status) {
+    case B64_OK: return "ok";
+    case B64_ERR_INVALID_CHAR: return "invalid character";
+    case B64_ERR_LENGTH: return "length not a multiple of 4";
+    case B64_ERR_ARG: return "invalid argument";
+    case B64_ERR_CUDA: return "CUDA error";
+    case B64_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+const char *b64_build_info(void) { return "libb64gpu sm_100a (tcgen-free byte codec; TMA bulk I/O)"; }
+
+}  // extern "C"
