@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""bench.py -- base64 encode + validating decode throughput on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` (torchrun
+for N > 1) prints ONE JSON line on rank 0.
+
+Workload (default, BASELINE.json configs[4] = "C5"): 32 GiB of seeded
+random bytes split on 3-byte boundaries over the N ranks (b64_shard).  One
+step = the whole hot path over the rank's shard: encode its bytes (SURVEY.md
+§8 rows a1-a5), validating decode of the produced text (rows a6-a12, the
+last rank applies the final-quad rules) and -- for N > 1 -- the result
+exchange (int64 MIN all-reduce of the error offset + all-gather of output
+lengths over NCCL).  value = (encode input bytes + decode input chars) of all
+ranks x K / max-over-ranks device time, in GB/s (1e9).  Inputs are far larger
+than L2 (126 MB), so no flush is needed between steps.  ``--workload c3``
+runs config 3 (1 GiB + 2 bytes on every rank) instead; ``--workload c2``
+the batched 10,000-message config.
+
+``--impl reference`` times the CPU oracle (the only "reference" this paper
+has: no runnable code exists) on the host cores on bounded
+samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "base64 encode/decode GB/s (input bytes) per GPU and % of HBM roofline, 1-8 B200"
+FALLBACK_HBM_GBS = 6650.0
+
+
+# ------------------------------------------------------------------ utils
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count(), len(os.sched_getaffinity(0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw",
+              "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=1)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_threads_bench(x, reps_min_s=1.0, threads=None):
+    """Time the scalar CPU oracle (encode, then decode of its output) on the
+    host cores; the buffer is split on 3-byte boundaries into one chunk per
+    thread (ctypes releases the GIL).  Returns (GB/s of input bytes, cores,
+    bytes_in, seconds)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+
+    T = threads or len(os.sched_getaffinity(0))
+    n = x.size
+    q = (n + 2) // 3
+    bounds = [(min(3 * (q * r // T), n), min(3 * (q * (r + 1) // T), n)) for r in range(T)]
+    texts = [np.empty(4 * ((e - b + 2) // 3), dtype=np.uint8) for b, e in bounds]
+    outs = [np.empty(max(3 * (t.size // 4), 1), dtype=np.uint8) for t in texts]
+
+    def job(i):
+        b, e = bounds[i]
+        oracle.encode_into(x[b:e], texts[i])
+        oracle.decode_into(texts[i], outs[i])
+
+    oracle.build()
+    m = sum(t.size for t in texts)
+    with ThreadPoolExecutor(T) as ex:
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            list(ex.map(job, range(T)))
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= reps_min_s:
+                break
+    return (n + m) * reps / el / 1e9, T, (n + m) * reps, el
+
+
+# ------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1704_00605_b200 as b64
+    from inputs import workloads as W
+    from inputs.gpu_gen import fill
+    from paper_1704_00605_b200.dist import INT64_MAX
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    b64.load_library()
+    stream = torch.cuda.current_stream(dev)
+
+    wl = args.workload
+    if wl == "c5":
+        total, seed = W.C5_N, W.C5_SEED
+        begin, end = b64.b64_shard(total, 3, world, rank)
+        scaling = "strong"
+        wdesc = "C5: 32 GiB uniform random bytes (seed 5) split on 3-byte boundaries over the ranks; encode + validating decode"
+    elif wl == "c3":
+        total, seed = W.C3_N, W.C3_SEED
+        begin, end = 0, total
+        scaling = "weak"
+        wdesc = "C3: 1 GiB + 2 uniform random bytes (seed 2) per rank; encode + validating decode"
+    else:
+        raise SystemExit(f"unknown workload {wl}")
+    n = end - begin
+    m = b64.b64_encoded_len(n)
+    final = rank == world - 1 or wl != "c5"
+
+    x = torch.empty(n, dtype=torch.uint8, device=dev)
+    fill(x, seed, begin)
+    t = torch.empty(m, dtype=torch.uint8, device=dev)
+    y = torch.empty(max(b64.b64_decoded_max_len(m), 1), dtype=torch.uint8, device=dev)
+    res = b64.result_tensor(dev)
+    lib = b64.load_library()
+    import ctypes
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    xp, tp, yp, rp = x.data_ptr(), t.data_ptr(), y.data_ptr(), res.data_ptr()
+
+    err_t = torch.empty(1, dtype=torch.int64, device=dev)
+    lens_parts = [torch.empty(1, dtype=torch.int64, device=dev) for _ in range(world)]
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        rc = lib.b64_encode(xp, n, tp, sptr)
+        if rc < 0:
+            raise RuntimeError(f"encode rc={rc}")
+        if ev is not None:
+            ev[1].record(stream)
+        rc = lib.b64_decode_shard_async(tp, m, 1 if final else 0, yp, rp, sptr)
+        if rc < 0:
+            raise RuntimeError(f"decode rc={rc}")
+        if ev is not None:
+            ev[2].record(stream)
+        if world > 1:
+            # result exchange: global error offset (MIN) + output lengths (gather)
+            e = res[1:2]
+            torch.where(e >= 0, e + begin, torch.full_like(e, INT64_MAX), out=err_t)
+            dist.all_reduce(err_t, op=dist.ReduceOp.MIN)
+            dist.all_gather(lens_parts, res[0:1])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    # correctness guard of the measured configuration (cheap, outside timing)
+    ol, ep, st, _ = b64.unpack_result(res)
+    assert st == 0 and ep == -1 and ol == n, (st, ep, ol)
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    time.sleep(0.15)
+    t_start.record(stream)
+    for k in range(K):
+        step(evs[k])
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    ms_total = t_start.elapsed_time(t_end)
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / K
+    dec_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / K
+    ms = torch.tensor([ms_total, enc_ms, dec_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_total, enc_ms, dec_ms = ms.tolist()
+
+    tot_n = total if wl == "c5" else total * world
+    tot_m = b64.b64_encoded_len(total) if wl == "c5" else b64.b64_encoded_len(total) * world
+    value = (tot_n + tot_m) * K / (ms_total / 1e3) / 1e9
+
+    hbm, hbm_src = peaks()
+    enc_bytes = n + m           # algorithmic bytes per encode launch (read n, write 4*ceil(n/3))
+    dec_bytes = m + n           # per decode launch (read m chars, write n bytes)
+    enc_gbs = enc_bytes / (enc_ms / 1e3) / 1e9
+    dec_gbs = dec_bytes / (dec_ms / 1e3) / 1e9
+    dom = "decode" if dec_ms >= enc_ms else "encode"
+    ach = dec_gbs if dom == "decode" else enc_gbs
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        ent = tr.get(f"{wl}:{dom}") or tr.get(dom)
+        if ent:
+            traffic = ent.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+
+    # ---- e2e through the C ABI host-buffer entry points (rank-local sample)
+    e2e = None
+    if not args.no_e2e:
+        ns = min(n, args.e2e_bytes - args.e2e_bytes % 3) if n > args.e2e_bytes else n
+        ms_ = b64.b64_encoded_len(ns)
+        hx = torch.empty(ns, dtype=torch.uint8).pin_memory()
+        hx.copy_(x[:ns])
+        ht = torch.empty(ms_, dtype=torch.uint8).pin_memory()
+        hy = torch.empty(max(b64.b64_decoded_max_len(ms_), 1), dtype=torch.uint8).pin_memory()
+        for _ in range(1):
+            b64.b64_encode_host(hx, ht, x, t)
+            b64.b64_decode_host(ht, hy, t, y)
+        reps = args.e2e_steps
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            b64.b64_encode_host(hx, ht, x, t)
+            st_, ol_, ep_ = b64.b64_decode_host(ht, hy, t, y)
+        el = time.perf_counter() - t0
+        assert st_ == 0 and ol_ == ns
+        elt = torch.tensor([el], dtype=torch.float64, device=dev)
+        tot = torch.tensor([float(ns + ms_)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(elt, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        e2e = {"value": tot.item() * reps / elt.item() / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": ns + ms_, "d2h_bytes_per_step": ms_ + ns + 2 * 24,
+               "sample": f"{ns} bytes per rank (pinned host) -> b64_encode_host -> b64_decode_host, {reps} steps"}
+
+    # ---- CPU oracle on the host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        smp = min(n, args.cpu_sample)
+        smp -= smp % 3
+        xs = x[:smp].cpu().numpy()
+        gbs, cores, nbytes, el = oracle_threads_bench(xs, reps_min_s=args.cpu_seconds)
+        model, ncpu, naff = cpu_info()
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {smp} bytes of the rank-0 workload: oracle encode + decode of its text, "
+                         f"split on 3-byte boundaries over {cores} threads, {el:.1f} s wall",
+               "cpu_model": model, "cpu_count": ncpu}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_total / K, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic: counter-based SplitMix64 bytes (inputs/gen.py), generated on device",
+            "config": {"workload": wdesc, "bytes_per_rank": n, "chars_per_rank": m,
+                       "total_bytes": tot_n, "total_chars": tot_m,
+                       "parallelism": f"shard x{world}: no data-path collective; MIN all-reduce + length all-gather",
+                       "l2": "inputs larger than L2 (126 MB): no flush"},
+            "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel", "achieved": ach, "peak": hbm,
+                         "unit": "GB/s", "frac": ach / hbm, "traffic": traffic, "peak_source": hbm_src,
+                         "algorithmic_bytes_per_launch": dec_bytes if dom == "decode" else enc_bytes},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * K,
+            "gpu_launches_scope": "per rank: 1 encode_kernel + 1 decode_kernel per step",
+            "clocks": clocks,
+            "detail": {"encode_ms": enc_ms, "decode_ms": dec_ms,
+                       "encode_GBps_input": n / (enc_ms / 1e3) / 1e9,
+                       "decode_GBps_input": m / (dec_ms / 1e3) / 1e9,
+                       "encode_roofline_frac": enc_gbs / hbm, "decode_roofline_frac": dec_gbs / hbm,
+                       "encode_hbm_GBps": enc_gbs, "decode_hbm_GBps": dec_gbs},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# -------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from inputs import workloads as W
+    from inputs.gen import splitmix_bytes
+
+    seed = W.C5_SEED if args.workload == "c5" else W.C3_SEED
+    smp = args.cpu_sample - args.cpu_sample % 3
+    x = splitmix_bytes(seed, 0, smp)
+    for _ in range(args.warmup):
+        oracle_threads_bench(x, reps_min_s=0.0)
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        gbs, cores, nbytes, el = oracle_threads_bench(x, reps_min_s=0.0)
+        vals.append(gbs)
+        secs += el
+    value = statistics.mean(vals)
+    model, ncpu, _ = cpu_info()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+        "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic: counter-based SplitMix64 bytes (inputs/gen.py)",
+        "config": {"workload": f"{args.workload.upper()} sample: first {smp} bytes per step (oracle encode + decode)"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{smp} bytes per step, split on 3-byte boundaries over {cores} threads",
+                         "cpu_model": model, "cpu_count": ncpu},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c3"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-bytes", type=int, default=3 << 28)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=48 << 20)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours" and os.environ.get("B64_BENCH_ALLOW_FEW_WARMUP") != "1":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
