@@ -14,14 +14,23 @@ constexpr int kThreads = kNT + 32;          // + one producer (TMA) warp
 constexpr int kStagesIn = 4;                // input ring depth
 constexpr int kStagesOut = 2;               // output staging depth
 
-// Encode: each compute thread turns 12 bytes (4 groups) into 16 chars per pass.
-constexpr int kEncPasses = 2;
-constexpr int kEncIn = kNT * 12 * kEncPasses;   // 6144 input bytes per tile
-constexpr int kEncOut = kNT * 16 * kEncPasses;  // 8192 output chars per tile
-// Decode: each compute thread turns 16 chars (4 quads) into 12 bytes per pass.
-constexpr int kDecPasses = 2;
-constexpr int kDecIn = kNT * 16 * kDecPasses;   // 8192 input chars per tile
-constexpr int kDecOut = kNT * 12 * kDecPasses;  // 6144 output bytes per tile
+// Encode: each compute thread turns 12 bytes (4 groups) into 16 chars per
+// pass; decode: 16 chars (4 quads) into 12 bytes per pass.  A tile is P
+// passes of the 256 compute threads.
+template <int P>
+struct EncG {
+  static constexpr int kPasses = P;
+  static constexpr int kIn = kNT * 12 * P;   // input bytes per tile
+  static constexpr int kOut = kNT * 16 * P;  // output chars per tile
+};
+template <int P>
+struct DecG {
+  static constexpr int kPasses = P;
+  static constexpr int kIn = kNT * 16 * P;   // input chars per tile
+  static constexpr int kOut = kNT * 12 * P;  // output bytes per tile
+};
+constexpr int kSinglePasses = 4;  // single buffer: 12 KiB in / 16 KiB out (encode)
+constexpr int kBatchPasses = 1;   // batched: small tiles for data-URI-sized messages
 
 constexpr int round_up_c(int x, int a) { return (x + a - 1) / a * a; }
 
@@ -159,19 +168,20 @@ __device__ __forceinline__ void set_byte16(uint32_t (&c)[4], int i, uint32_t v) 
 // Alg 1's tail is handled by the one thread whose 12-byte run
 // crosses L: missing bytes are zero (so the emitted fields equal
 // (s_i*16) mod 64 and (s_{i+1}*4) mod 64) and '=' pads are substituted.
-template <int IA, int OA>
+// FULL: the tile has exactly EncG<P>::kIn bytes (no tail / inactive-lane checks).
+template <int IA, int OA, bool FULL, int P>
 __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *sout,
                                             const uint8_t *tab, int tid, int lane) {
 #pragma unroll
-  for (int pass = 0; pass < kEncPasses; ++pass) {
+  for (int pass = 0; pass < P; ++pass) {
     const int bo = pass * (kNT * 12) + tid * 12;
     const int co = pass * (kNT * 16) + tid * 16;
-    const bool active = bo < L;
-    if (!__any_sync(0xffffffffu, active)) break;
+    const bool active = FULL || bo < L;
+    if (!FULL && !__any_sync(0xffffffffu, active)) break;
     uint32_t w[3];
     load_words<(IA >= 4 ? 4 : 1), 3>(sin + bo, w);
     const int rem = L - bo;
-    const bool partial = active && rem < 12;
+    const bool partial = !FULL && active && rem < 12;
     if (partial) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -204,21 +214,22 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
 // per-char mask, final-quad '=' rules (reading R-pad), first bad offset,
 // warp __reduce_min_sync.  Returns (lane 0 meaningful) the tile-relative
 // minimum error offset, or 0xFFFFFFFF.
-template <int IA, int OA>
+// FULL: the tile has exactly DecG<P>::kIn chars and is not a final tile.
+template <int IA, int OA, bool FULL, int P>
 __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8_t *sout,
                                                 const uint8_t *tab, int tid, int lane,
                                                 bool final_tile, uint32_t ch2, uint32_t ch1) {
   uint32_t errmin = 0xFFFFFFFFu;
 #pragma unroll
-  for (int pass = 0; pass < kDecPasses; ++pass) {
+  for (int pass = 0; pass < P; ++pass) {
     const int co = pass * (kNT * 16) + tid * 16;
     const int bo = pass * (kNT * 12) + tid * 12;
-    const bool active = co < L;
-    if (!__any_sync(0xffffffffu, active)) break;
+    const bool active = FULL || co < L;
+    if (!FULL && !__any_sync(0xffffffffu, active)) break;
     uint32_t w[4];
     load_words<IA, 4>(sin + co, w);
     const int rem = L - co;
-    if (!active || rem < 16) {
+    if (!FULL && (!active || rem < 16)) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (!active || 4 * k >= rem) w[k] = 0x41414141u;  // "AAAA": ignored filler
@@ -243,7 +254,7 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
         for (int j = 0; j < 16; ++j) mask |= ((v[j] >> 7) & 1u) << j;
         // Final quad of the stream (reading R-pad): '=' allowed at m-2 and
         // m-1, and '=' at m-2 forces '=' at m-1; '=' contributes value 0.
-        if (final_tile && co + 16 >= L && co < L) {
+        if (!FULL && final_tile && co + 16 >= L && co < L) {
           const int j1 = L - 1 - co, j2 = L - 2 - co;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {

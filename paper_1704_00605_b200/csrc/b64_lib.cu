@@ -35,10 +35,17 @@ struct alignas(128) Smem {
   TileDesc desc[kStagesIn];
   uint64_t full[kStagesIn];
   uint64_t empty[kStagesIn];
-  alignas(16) uint8_t table[256];
 };
-using EncSmem = Smem<kEncIn, kEncOut>;
-using DecSmem = Smem<kDecIn, kDecOut>;
+template <bool BATCH>
+using EncGeo = EncG<BATCH ? kBatchPasses : kSinglePasses>;
+template <bool BATCH>
+using DecGeo = DecG<BATCH ? kBatchPasses : kSinglePasses>;
+template <bool BATCH>
+using EncSmem = Smem<EncGeo<BATCH>::kIn, EncGeo<BATCH>::kOut>;
+template <bool BATCH>
+using DecSmem = Smem<DecGeo<BATCH>::kIn, DecGeo<BATCH>::kOut>;
+using EncS1 = EncGeo<false>;  // single-buffer tile geometry
+using DecS1 = DecGeo<false>;
 
 struct DecWs {                 // per-(device, stream) decode scratch (self-resetting)
   unsigned long long errkey;   // min error offset, ~0 = none
@@ -49,11 +56,11 @@ struct DecWs {                 // per-(device, stream) decode scratch (self-rese
 // ------------------------------------------------- tile descriptors ---
 __device__ __forceinline__ TileDesc enc_single_desc(int64_t j, int64_t n) {
   TileDesc d;
-  d.src = j * kEncIn;
-  d.dst = j * kEncOut;
+  d.src = j * EncS1::kIn;
+  d.dst = j * EncS1::kOut;
   d.rel = d.src;
   const int64_t left = n - d.src;
-  d.len = static_cast<int32_t>(left < kEncIn ? left : kEncIn);
+  d.len = static_cast<int32_t>(left < EncS1::kIn ? left : EncS1::kIn);
   d.msg = 0;
   d.flags = 0;
   d.ntiles = 0;
@@ -63,11 +70,11 @@ __device__ __forceinline__ TileDesc enc_single_desc(int64_t j, int64_t n) {
 __device__ __forceinline__ TileDesc dec_single_desc(int64_t j, int64_t ntiles, int64_t chars,
                                                     bool final_pad_rules) {
   TileDesc d;
-  d.src = j * kDecIn;
-  d.dst = j * kDecOut;
+  d.src = j * DecS1::kIn;
+  d.dst = j * DecS1::kOut;
   d.rel = d.src;
   const int64_t left = chars - d.src;
-  d.len = static_cast<int32_t>(left < kDecIn ? left : kDecIn);
+  d.len = static_cast<int32_t>(left < DecS1::kIn ? left : DecS1::kIn);
   d.msg = 0;
   d.flags = (final_pad_rules && j == ntiles - 1) ? kFlagFinal : 0;
   d.ntiles = 0;
@@ -155,11 +162,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                   int64_t ntiles_arg, const TileDesc *__restrict__ descs,
                   const int64_t *__restrict__ ntiles_dev) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  EncSmem &S = *reinterpret_cast<EncSmem *>(smem_raw);
+  using G = EncGeo<BATCH>;
+  EncSmem<BATCH> &S = *reinterpret_cast<EncSmem<BATCH> *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = BATCH ? *ntiles_dev : ntiles_arg;
+  // Static (not dynamic) shared table: LDS addressing is [index + immediate].
+  __shared__ alignas(16) uint8_t s_tab[64];
 
-  if (tid < 64) S.table[tid] = static_cast<uint8_t>(ascii_of(tid));  // Table I / II
+  if (tid < 64) s_tab[tid] = static_cast<uint8_t>(ascii_of(tid));  // Table I / II
   if (tid == 0) {
     for (int s = 0; s < kStagesIn; ++s) {
       mbar_init(&S.full[s], 1);
@@ -183,7 +193,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
     uint8_t *gdst = out + d.dst;
     const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
-    encode_tile<IA, OA>(S.in[s] + imis, d.len, S.out[so] + omis, S.table, tid, lane);
+    if (d.len == G::kIn)
+      encode_tile<IA, OA, true, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, s_tab, tid, lane);
+    else
+      encode_tile<IA, OA, false, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, s_tab, tid, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[s]);
     fence_proxy_async_smem();
@@ -233,14 +246,16 @@ __global__ void __launch_bounds__(kThreads, 2)
                   int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
                   int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  DecSmem &S = *reinterpret_cast<DecSmem *>(smem_raw);
+  using G = DecGeo<BATCH>;
+  DecSmem<BATCH> &S = *reinterpret_cast<DecSmem<BATCH> *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = BATCH ? *ntiles_dev : ntiles_arg;
   const int64_t chars = BATCH ? 0 : 4 * (m / 4);
   const bool pad_rules = final_shard != 0 && (m % 4) == 0;
 
   // Inverse map A: invalid everywhere, then A(B(v)) = v.
-  if (tid < 256) S.table[tid] = kInvalid;
+  __shared__ alignas(16) uint8_t s_tab[256];
+  if (tid < 256) s_tab[tid] = kInvalid;
   if (tid == 0) {
     for (int s = 0; s < kStagesIn; ++s) {
       mbar_init(&S.full[s], 1);
@@ -249,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid < 64) S.table[ascii_of(tid)] = static_cast<uint8_t>(tid);
+  if (tid < 64) s_tab[ascii_of(tid)] = static_cast<uint8_t>(tid);
   __syncthreads();
 
   if (warp == kWarpsC) {
@@ -276,7 +291,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       pads = ch1 == '=' ? (ch2 == '=' ? 2 : 1) : 0;
     }
     const uint32_t werr =
-        decode_tile<IA, OA>(sin, d.len, S.out[so] + omis, S.table, tid, lane, fin, ch2, ch1);
+        (d.len == G::kIn && !fin)
+            ? decode_tile<IA, OA, true, G::kPasses>(sin, d.len, S.out[so] + omis, s_tab, tid, lane,
+                                                    false, 0, 0)
+            : decode_tile<IA, OA, false, G::kPasses>(sin, d.len, S.out[so] + omis, s_tab, tid, lane,
+                                                     fin, ch2, ch1);
     __syncwarp();
     if (lane == 0) {
       mbar_arrive(&S.empty[s]);
@@ -413,7 +432,7 @@ __global__ void __launch_bounds__(kPlanThreads)
                 int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
   __shared__ int64_t sh[66];
   const int64_t cap = hdr->capacity;
-  constexpr int TILE = DECODE ? kDecIn : kEncIn;
+  constexpr int TILE = DECODE ? DecGeo<true>::kIn : EncGeo<true>::kIn;
   int64_t carry_out = 0, carry_tiles = 0;
   for (int64_t base = 0; base < k; base += static_cast<int64_t>(kPlanThreads) * kPlanItems) {
     const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * kPlanItems;
@@ -579,12 +598,12 @@ bool device_setup(int *dev_out, int *sms_out) {
       return false;
     for (auto &row : enc_table)
       for (auto f : row)
-        if (set_smem(f, sizeof(EncSmem)) != cudaSuccess) return false;
+        if (set_smem(f, sizeof(EncSmem<false>)) != cudaSuccess) return false;
     for (auto &row : dec_table)
       for (auto f : row)
-        if (set_smem(f, sizeof(DecSmem)) != cudaSuccess) return false;
-    if (set_smem(encode_kernel<1, 1, true>, sizeof(EncSmem)) != cudaSuccess) return false;
-    if (set_smem(decode_kernel<1, 1, true>, sizeof(DecSmem)) != cudaSuccess) return false;
+        if (set_smem(f, sizeof(DecSmem<false>)) != cudaSuccess) return false;
+    if (set_smem(encode_kernel<1, 1, true>, sizeof(EncSmem<true>)) != cudaSuccess) return false;
+    if (set_smem(decode_kernel<1, 1, true>, sizeof(DecSmem<true>)) != cudaSuccess) return false;
     di.attrs_set = true;
   }
   *dev_out = dev;
@@ -618,10 +637,10 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   const int64_t chars = 4 * (m / 4);
-  const int64_t ntiles = (chars + kDecIn - 1) / kDecIn;
+  const int64_t ntiles = (chars + DecS1::kIn - 1) / DecS1::kIn;
   const int64_t grid = grid_for(ntiles, sms);
   DecFn f = dec_table[align_class(d_in)][align_class(d_out)];
-  f<<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem), stream>>>(
+  f<<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem<false>), stream>>>(
       d_in, m, d_out, ntiles, final_shard, ws, d_result, nullptr, nullptr, nullptr, nullptr,
       nullptr, nullptr, nullptr, nullptr);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
@@ -629,7 +648,7 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
 
 size_t ws_layout(int64_t k, int64_t total_in, int direction, size_t *off_descs, size_t *off_done,
                  int64_t *cap) {
-  const int64_t tile = direction ? kDecIn : kEncIn;
+  const int64_t tile = direction ? DecGeo<true>::kIn : EncGeo<true>::kIn;
   const int64_t c = (total_in > 0 ? total_in / tile : 0) + k + 1;
   size_t o = 256;  // PlanHeader
   *off_descs = o;
@@ -658,10 +677,10 @@ int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t 
   if (n == 0) return 0;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
-  const int64_t ntiles = (n + kEncIn - 1) / kEncIn;
+  const int64_t ntiles = (n + EncS1::kIn - 1) / EncS1::kIn;
   const int64_t grid = grid_for(ntiles, sms);
   EncFn f = enc_table[align_class(d_in)][align_class(d_out)];
-  f<<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem), stream>>>(d_in, n, d_out, ntiles,
+  f<<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem<false>), stream>>>(d_in, n, d_out, ntiles,
                                                                           nullptr, nullptr);
   if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
   return 4 * ((n + 2) / 3);
@@ -740,15 +759,15 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
                                                         nullptr, nullptr, nullptr, done);
   }
   if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
-  const int64_t tile = direction ? kDecIn : kEncIn;
+  const int64_t tile = direction ? DecGeo<true>::kIn : EncGeo<true>::kIn;
   const int64_t max_tiles = total_in / tile + k;
   const int64_t grid = grid_for(max_tiles, sms);
   if (direction) {
-    decode_kernel<1, 1, true><<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem), stream>>>(
+    decode_kernel<1, 1, true><<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem<true>), stream>>>(
         d_in, 0, d_out, 0, 1, nullptr, nullptr, descs, &hdr->ntiles, d_in_off, d_out_off,
         d_err_pos, d_out_len, d_status, done);
   } else {
-    encode_kernel<1, 1, true><<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem), stream>>>(
+    encode_kernel<1, 1, true><<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem<true>), stream>>>(
         d_in, 0, d_out, 0, descs, &hdr->ntiles);
   }
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;

@@ -30,16 +30,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Block until the phase with the given parity has completed.
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+// Block until the phase with the given parity has completed.  try_wait
+// suspends the thread in hardware for up to `hint_ns` before re-polling, so
+// a waiting producer warp does not burn issue slots of the compute warps.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, uint32_t hint_ns = 20000) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(hint_ns)
       : "memory");
 }
 

@@ -17,8 +17,8 @@ from tests.gpu_util import DEV, empty_dev, host, to_dev
 pytestmark = pytest.mark.gpu
 
 ALPHABET = (string.ascii_uppercase + string.ascii_lowercase + string.digits + "+/").encode()
-ENC_TILE = 6144      # input bytes per encode tile (b64_codec.cuh kEncIn)
-DEC_TILE = 8192      # input chars per decode tile (kDecIn)
+ENC_TILE = 12288     # input bytes per single-buffer encode tile (EncG<kSinglePasses>::kIn)
+DEC_TILE = 16384     # input chars per single-buffer decode tile (DecG<kSinglePasses>::kIn)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -145,7 +145,7 @@ def test_decode_every_byte_at_every_position_of_a_block():
     of a 3-tile buffer, at the 16-char thread seams and the tile seam."""
     x = splitmix_bytes(108, 0, 3 * DEC_TILE)
     t = oracle.encode(x)          # 4 * DEC_TILE chars, no padding
-    positions = list(range(4096, 4096 + 64)) + [15, 16, 8191, 8192, 8193, 16383, t.size - 1, t.size - 2]
+    positions = list(range(4096, 4096 + 64)) + [15, 16, 3071, 3072, 16383, 16384, 16385, 32767, t.size - 1, t.size - 2]
     d = to_dev(t)
     cap = b64.b64_decoded_max_len(t.size)
     _, out = empty_dev(cap)
