@@ -57,6 +57,21 @@ __device__ __forceinline__ uint32_t ascii_of(uint32_t v) {
   return static_cast<uint32_t>(static_cast<int>(v) + off);
 }
 
+// The two lookup tables live in static shared memory and are indexed by name
+// so that each lookup compiles to one LDS.U8 [idx + UR] (uniform base, no
+// per-lookup address add).
+__shared__ alignas(256) uint8_t g_dec_tab[256];  // A: byte -> 6-bit value | kInvalid
+__shared__ alignas(64) uint8_t g_enc_tab[64];    // B: 6-bit value -> ASCII (Table I)
+
+// Decode lookup of byte `sel` (0..3) of word w: g_dec_tab is 256-byte aligned,
+// so the shared address is the table base with its low byte replaced by the
+// character -- one PRMT/LOP3 forms the address, one LDS.U8 reads the entry.
+__device__ __forceinline__ uint32_t lds_u8(uint32_t saddr) {
+  uint32_t v;
+  asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+
 // ---------------------------------------------------- smem word access ---
 // Load N little-endian words of the stream starting at smem byte address p.
 // ALIGN: guaranteed alignment of p (16, 4 or 1); ALIGN 1 realigns with
@@ -133,24 +148,23 @@ __device__ __forceinline__ void store_words(uint8_t *p, const uint32_t (&D)[N], 
 // 17..12, 11..6, 5..0 of x; each is mapped through the 64-entry smem table B
 // and the four characters are packed little-endian (first char = byte 0).
 template <bool TOPZERO>
-__device__ __forceinline__ uint32_t enc_group(uint32_t x, const uint8_t *tab) {
+__device__ __forceinline__ uint32_t enc_group(uint32_t x) {
   const uint32_t i0 = TOPZERO ? (x >> 18) : ((x >> 18) & 63u);
   const uint32_t i1 = (x >> 12) & 63u;
   const uint32_t i2 = (x >> 6) & 63u;
   const uint32_t i3 = x & 63u;
-  const uint32_t c0 = tab[i0], c1 = tab[i1], c2 = tab[i2], c3 = tab[i3];
+  const uint32_t c0 = g_enc_tab[i0], c1 = g_enc_tab[i1], c2 = g_enc_tab[i2], c3 = g_enc_tab[i3];
   return __byte_perm(__byte_perm(c0, c1, 0x3340), __byte_perm(c2, c3, 0x3340), 0x5410);
 }
 
 // 12 input bytes (w0..w2, little-endian) -> 16 output chars (c0..c3).
 // __byte_perm reorders each 3-byte group big-endian (the GPU counterpart of
 // the paper's vpshufb step in enc_reshuffle).
-__device__ __forceinline__ void encode12(const uint32_t (&w)[3], uint32_t (&c)[4],
-                                         const uint8_t *tab) {
-  c[0] = enc_group<true>(__byte_perm(w[0], 0u, 0x4012), tab);    // b0 b1 b2
-  c[1] = enc_group<false>(__byte_perm(w[0], w[1], 0x3345), tab);  // b3 b4 b5
-  c[2] = enc_group<false>(__byte_perm(w[1], w[2], 0x2234), tab);  // b6 b7 b8
-  c[3] = enc_group<true>(__byte_perm(w[2], 0u, 0x4123), tab);    // b9 b10 b11
+__device__ __forceinline__ void encode12(const uint32_t (&w)[3], uint32_t (&c)[4]) {
+  c[0] = enc_group<true>(__byte_perm(w[0], 0u, 0x4012));    // b0 b1 b2
+  c[1] = enc_group<false>(__byte_perm(w[0], w[1], 0x3345));  // b3 b4 b5
+  c[2] = enc_group<false>(__byte_perm(w[1], w[2], 0x2234));  // b6 b7 b8
+  c[3] = enc_group<true>(__byte_perm(w[2], 0u, 0x4123));    // b9 b10 b11
 }
 
 // Replace byte i (0..15) of the 4-word vector with value v.
@@ -170,8 +184,8 @@ __device__ __forceinline__ void set_byte16(uint32_t (&c)[4], int i, uint32_t v) 
 // (s_i*16) mod 64 and (s_{i+1}*4) mod 64) and '=' pads are substituted.
 // FULL: the tile has exactly EncG<P>::kIn bytes (no tail / inactive-lane checks).
 template <int IA, int OA, bool FULL, int P>
-__device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *sout,
-                                            const uint8_t *tab, int tid, int lane) {
+__device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *sout, int tid,
+                                            int lane) {
 #pragma unroll
   for (int pass = 0; pass < P; ++pass) {
     const int bo = pass * (kNT * 12) + tid * 12;
@@ -191,7 +205,7 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
       }
     }
     uint32_t c[4];
-    encode12(w, c, tab);
+    encode12(w, c);
     if (partial) {
       const int left = rem % 3;           // 1 -> "xx==", 2 -> "xxx="
       if (left != 0) {
@@ -217,9 +231,10 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
 // FULL: the tile has exactly DecG<P>::kIn chars and is not a final tile.
 template <int IA, int OA, bool FULL, int P>
 __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8_t *sout,
-                                                const uint8_t *tab, int tid, int lane,
+                                                int tid, int lane,
                                                 bool final_tile, uint32_t ch2, uint32_t ch1) {
   uint32_t errmin = 0xFFFFFFFFu;
+  const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(g_dec_tab));
 #pragma unroll
   for (int pass = 0; pass < P; ++pass) {
     const int co = pass * (kNT * 16) + tid * 16;
@@ -238,14 +253,14 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
     uint32_t acc = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      v[4 * k + 0] = tab[w[k] & 0xFFu];
-      v[4 * k + 1] = tab[__byte_perm(w[k], 0u, 0x4441)];
-      v[4 * k + 2] = tab[__byte_perm(w[k], 0u, 0x4442)];
-      v[4 * k + 3] = tab[w[k] >> 24];
+      v[4 * k + 0] = lds_u8((w[k] & 0xFFu) | tb);
+      v[4 * k + 1] = lds_u8(__byte_perm(w[k], tb, 0x7651));
+      v[4 * k + 2] = lds_u8(__byte_perm(w[k], tb, 0x7652));
+      v[4 * k + 3] = lds_u8(__byte_perm(w[k], tb, 0x7653));
       acc |= v[4 * k + 0] | v[4 * k + 1];
       acc |= v[4 * k + 2] | v[4 * k + 3];
     }
-    const bool bad = (acc & 0x80u) != 0;
+    const uint32_t bad = acc & 0x80u;
     if (__any_sync(0xffffffffu, bad)) {
       uint32_t pos = 0xFFFFFFFFu;
       if (bad) {

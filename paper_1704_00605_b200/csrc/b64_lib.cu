@@ -166,10 +166,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   EncSmem<BATCH> &S = *reinterpret_cast<EncSmem<BATCH> *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = BATCH ? *ntiles_dev : ntiles_arg;
-  // Static (not dynamic) shared table: LDS addressing is [index + immediate].
-  __shared__ alignas(16) uint8_t s_tab[64];
-
-  if (tid < 64) s_tab[tid] = static_cast<uint8_t>(ascii_of(tid));  // Table I / II
+  if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid));  // Table I / II
   if (tid == 0) {
     for (int s = 0; s < kStagesIn; ++s) {
       mbar_init(&S.full[s], 1);
@@ -194,9 +191,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint8_t *gdst = out + d.dst;
     const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
     if (d.len == G::kIn)
-      encode_tile<IA, OA, true, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, s_tab, tid, lane);
+      encode_tile<IA, OA, true, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, tid, lane);
     else
-      encode_tile<IA, OA, false, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, s_tab, tid, lane);
+      encode_tile<IA, OA, false, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, tid, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[s]);
     fence_proxy_async_smem();
@@ -254,8 +251,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const bool pad_rules = final_shard != 0 && (m % 4) == 0;
 
   // Inverse map A: invalid everywhere, then A(B(v)) = v.
-  __shared__ alignas(16) uint8_t s_tab[256];
-  if (tid < 256) s_tab[tid] = kInvalid;
+  if (tid < 256) g_dec_tab[tid] = kInvalid;
   if (tid == 0) {
     for (int s = 0; s < kStagesIn; ++s) {
       mbar_init(&S.full[s], 1);
@@ -264,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid < 64) s_tab[ascii_of(tid)] = static_cast<uint8_t>(tid);
+  if (tid < 64) g_dec_tab[ascii_of(tid)] = static_cast<uint8_t>(tid);
   __syncthreads();
 
   if (warp == kWarpsC) {
@@ -292,9 +288,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     const uint32_t werr =
         (d.len == G::kIn && !fin)
-            ? decode_tile<IA, OA, true, G::kPasses>(sin, d.len, S.out[so] + omis, s_tab, tid, lane,
+            ? decode_tile<IA, OA, true, G::kPasses>(sin, d.len, S.out[so] + omis, tid, lane,
                                                     false, 0, 0)
-            : decode_tile<IA, OA, false, G::kPasses>(sin, d.len, S.out[so] + omis, s_tab, tid, lane,
+            : decode_tile<IA, OA, false, G::kPasses>(sin, d.len, S.out[so] + omis, tid, lane,
                                                      fin, ch2, ch1);
     __syncwarp();
     if (lane == 0) {
