@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   int it = 0;
   for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
     const int s = it % kStagesIn, so = it % kStagesOut;
-    mbar_wait(&S.full[s], (it / kStagesIn) & 1);
+    mbar_wait_spin(&S.full[s], (it / kStagesIn) & 1);
     const TileDesc d = S.desc[s];
     const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
     uint8_t *gdst = out + d.dst;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   int it = 0;
   for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
     const int s = it % kStagesIn, so = it % kStagesOut;
-    mbar_wait(&S.full[s], (it / kStagesIn) & 1);
+    mbar_wait_spin(&S.full[s], (it / kStagesIn) & 1);
     const TileDesc d = S.desc[s];
     const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
     uint8_t *gdst = out + d.dst;

@@ -45,6 +45,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, uint32
       : "memory");
 }
 
+// Consumer-side wait: plain try_wait loop (no suspend hint), the data
+// normally lands within a few hundred cycles of being needed.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // 1-D bulk copy global -> shared, completion signalled on `bar` (complete_tx).
 // src and dst 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes,
