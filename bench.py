@@ -275,7 +275,7 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        ent = tr.get(f"{wl}:{dom}") or tr.get(dom)
+        ent = tr.get(f"{wl}:{dom}")
         if ent:
             traffic = ent.get("dram_bytes_per_launch")
     except (OSError, ValueError):

@@ -10,6 +10,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libb64gpu.so")
+# Experiments only (tools/sweep.py): load a variant build of the same library.
+if os.environ.get("B64GPU_LIB"):
+    _LIB_PATH = os.environ["B64GPU_LIB"]
 
 B64_OK = 0
 B64_ERR_INVALID_CHAR = 1

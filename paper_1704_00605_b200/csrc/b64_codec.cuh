@@ -8,11 +8,36 @@
 namespace b64 {
 
 // ------------------------------------------------------------ geometry ---
-constexpr int kWarpsC = 8;                  // compute warps per CTA
+// Tunables (compile-time; the defaults are the measured best, see
+// DESIGN.md §6 and tools/sweep.py).
+#ifndef B64_WARPS_C
+#define B64_WARPS_C 8
+#endif
+#ifndef B64_STAGES_IN
+#define B64_STAGES_IN 4
+#endif
+#ifndef B64_STAGES_OUT
+#define B64_STAGES_OUT 2
+#endif
+#ifndef B64_SINGLE_PASSES
+#define B64_SINGLE_PASSES 4
+#endif
+#ifndef B64_BATCH_PASSES
+#define B64_BATCH_PASSES 1
+#endif
+#ifndef B64_CTAS_PER_SM
+#define B64_CTAS_PER_SM 2
+#endif
+#ifndef B64_STORE_EVICT_FIRST
+#define B64_STORE_EVICT_FIRST 0
+#endif
+constexpr int kWarpsC = B64_WARPS_C;        // compute warps per CTA
 constexpr int kNT = kWarpsC * 32;           // compute threads per CTA
 constexpr int kThreads = kNT + 32;          // + one producer (TMA) warp
-constexpr int kStagesIn = 4;                // input ring depth
-constexpr int kStagesOut = 2;               // output staging depth
+constexpr int kStagesIn = B64_STAGES_IN;    // input ring depth
+constexpr int kStagesOut = B64_STAGES_OUT;  // output staging depth
+constexpr int kCtasPerSm = B64_CTAS_PER_SM;
+static_assert(kStagesOut >= 2, "output staging needs >= 2 slots");
 
 // Encode: each compute thread turns 12 bytes (4 groups) into 16 chars per
 // pass; decode: 16 chars (4 quads) into 12 bytes per pass.  A tile is P
@@ -29,8 +54,8 @@ struct DecG {
   static constexpr int kIn = kNT * 16 * P;   // input chars per tile
   static constexpr int kOut = kNT * 12 * P;  // output bytes per tile
 };
-constexpr int kSinglePasses = 4;  // single buffer: 12 KiB in / 16 KiB out (encode)
-constexpr int kBatchPasses = 1;   // batched: small tiles for data-URI-sized messages
+constexpr int kSinglePasses = B64_SINGLE_PASSES;  // single buffer: 12 KiB in / 16 KiB out (encode)
+constexpr int kBatchPasses = B64_BATCH_PASSES;    // batched: small tiles for data-URI-sized messages
 
 constexpr int round_up_c(int x, int a) { return (x + a - 1) / a * a; }
 

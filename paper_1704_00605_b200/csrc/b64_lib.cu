@@ -157,7 +157,7 @@ __device__ __forceinline__ void copy_out(uint8_t *gdst, const uint8_t *sbuf, int
 
 // ------------------------------------------------------ encode kernel ---
 template <int IA, int OA, bool BATCH>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     encode_kernel(const uint8_t *__restrict__ in, int64_t n, uint8_t *__restrict__ out,
                   int64_t ntiles_arg, const TileDesc *__restrict__ descs,
                   const int64_t *__restrict__ ntiles_dev) {
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     return;
   }
 
-  const uint64_t pol_out = policy_evict_normal();
+  const uint64_t pol_out = B64_STORE_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();
   int it = 0;
   for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
     const int s = it % kStagesIn, so = it % kStagesOut;
@@ -235,7 +235,7 @@ __device__ void finalize_single(const uint8_t *in, int64_t m, bool final_shard,
 }
 
 template <int IA, int OA, bool BATCH>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
                   int64_t ntiles_arg, int final_shard, DecWs *ws, b64_result *res,
                   const TileDesc *__restrict__ descs, const int64_t *__restrict__ ntiles_dev,
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     return;
   }
 
-  const uint64_t pol_out = policy_evict_normal();
+  const uint64_t pol_out = B64_STORE_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();
   int it = 0;
   for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
     const int s = it % kStagesIn, so = it % kStagesOut;
@@ -553,7 +553,7 @@ struct StreamWs {
 };
 std::map<std::pair<int, uintptr_t>, StreamWs> g_ws;
 
-int ctas_per_sm() { return 2; }
+int ctas_per_sm() { return kCtasPerSm; }
 
 template <class K>
 cudaError_t set_smem(K kernel, int bytes) {

@@ -1,0 +1,106 @@
+#!/usr/bin/env python
+"""A/B sweep of compile-time kernel tunables (b64_codec.cuh B64_* macros).
+
+  python tools/sweep.py build [names...]        # here (CPU): nvcc variants -> build/variants/
+  python tools/sweep.py run [--workload c5] [names...]   # on the GPU box (gpurun)
+
+Each variant is a full build of libb64gpu.so; `run` times it through
+bench.py (B64GPU_LIB points the binding at the variant) and prints one line
+per variant.  Results are evidence for the defaults chosen in b64_codec.cuh.
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "build", "variants")
+SRC = os.path.join(ROOT, "paper_1704_00605_b200", "csrc", "b64_lib.cu")
+
+VARIANTS = {
+    "base": {},
+    "store_ef": {"B64_STORE_EVICT_FIRST": 1},
+    "in3": {"B64_STAGES_IN": 3},
+    "in5": {"B64_STAGES_IN": 5},
+    "out3": {"B64_STAGES_OUT": 3},
+    "p2": {"B64_SINGLE_PASSES": 2},
+    "p2_in6": {"B64_SINGLE_PASSES": 2, "B64_STAGES_IN": 6},
+    "w4_c4": {"B64_WARPS_C": 4, "B64_CTAS_PER_SM": 4},
+    "w16_c1": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1},
+    "w12_c1_p4": {"B64_WARPS_C": 12, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 6},
+    "p8_c1": {"B64_SINGLE_PASSES": 8, "B64_CTAS_PER_SM": 1},
+}
+
+
+def build(names):
+    os.makedirs(OUT, exist_ok=True)
+    procs = []
+    for n in names:
+        defs = [f"-D{k}={v}" for k, v in VARIANTS[n].items()]
+        out = os.path.join(OUT, f"libb64gpu_{n}.so")
+        cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+               "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", *defs, "-o", out, SRC]
+        procs.append((n, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    for n, p in procs:
+        o, _ = p.communicate()
+        print(n, "ok" if p.returncode == 0 else "FAILED\n" + o)
+
+
+def run(names, workload, steps, reps):
+    rows = []
+    for r in range(reps):
+        for n in names:
+            lib = os.path.join(OUT, f"libb64gpu_{n}.so")
+            env = dict(os.environ, B64GPU_LIB=lib)
+            cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", workload, "--steps", str(steps),
+                   "--warmup", "3", "--no-e2e", "--no-cpu"]
+            p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+            line = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+            if p.returncode != 0 or not line:
+                print(f"{n:12} FAILED rc={p.returncode} {p.stderr[-300:]}", flush=True)
+                continue
+            d = json.loads(line[-1])
+            det = d["detail"]
+            row = {"variant": n, "rep": r, "value": d["value"], "enc_frac": det["encode_roofline_frac"],
+                   "dec_frac": det["decode_roofline_frac"], "sm_mhz": d["clocks"]["sm_mhz"],
+                   "reasons": d["clocks"]["reasons"]}
+            rows.append(row)
+            print(f"{n:12} rep{r} value {d['value']:8.1f} GB/s  enc {det['encode_roofline_frac']:.3f} "
+                  f"dec {det['decode_roofline_frac']:.3f}  sm {d['clocks']['sm_mhz']} {d['clocks']['reasons']}",
+                  flush=True)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"sweep_{workload}.json"), "w") as f:
+        json.dump(rows, f, indent=1)
+
+
+def main():
+    args = sys.argv[1:]
+    if not args:
+        print(__doc__)
+        return
+    cmd, rest = args[0], args[1:]
+    workload, steps, reps = "c5", 40, 1
+    names = []
+    i = 0
+    while i < len(rest):
+        if rest[i] == "--workload":
+            workload = rest[i + 1]
+            i += 2
+        elif rest[i] == "--steps":
+            steps = int(rest[i + 1])
+            i += 2
+        elif rest[i] == "--reps":
+            reps = int(rest[i + 1])
+            i += 2
+        else:
+            names.append(rest[i])
+            i += 1
+    names = names or list(VARIANTS)
+    if cmd == "build":
+        build(names)
+    else:
+        run(names, workload, steps, reps)
+
+
+if __name__ == "__main__":
+    main()
