@@ -232,7 +232,8 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     # correctness guard of the measured configuration (cheap, outside timing)
     ol, ep, st, _ = b64.unpack_result(res)
-    assert st == 0 and ep == -1 and ol == n, (st, ep, ol)
+    if os.environ.get("B64_BENCH_NOCHECK") != "1":   # skeleton variants only (tools/sweep.py)
+        assert st == 0 and ep == -1 and ol == n, (st, ep, ol)
 
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]

@@ -28,6 +28,9 @@ namespace b64 {
 #ifndef B64_CTAS_PER_SM
 #define B64_CTAS_PER_SM 2
 #endif
+#ifndef B64_SKELETON  // measurement only: move the bytes, skip the transform
+#define B64_SKELETON 0
+#endif
 #ifndef B64_STORE_EVICT_FIRST
 #define B64_STORE_EVICT_FIRST 0
 #endif
@@ -165,6 +168,14 @@ __device__ __forceinline__ void store_words(uint8_t *p, const uint32_t (&D)[N], 
   }
 }
 
+// 16-byte global store (STG.E.128).
+__device__ __forceinline__ void st_global_v4(uint8_t *p, const uint32_t (&c)[4]) {
+  *reinterpret_cast<uint4 *>(p) = make_uint4(c[0], c[1], c[2], c[3]);
+}
+__device__ __forceinline__ void st_global_v4(uint8_t *p, const uint4 &v) {
+  *reinterpret_cast<uint4 *>(p) = v;
+}
+
 // ------------------------------------------------------------- encode ---
 // One group (Alg 1 main loop body): x holds s_i<<16 | s_{i+1}<<8 |
 // s_{i+2} in its low 24 bits; TOPZERO says whether bits 24..31 are zero.
@@ -208,9 +219,13 @@ __device__ __forceinline__ void set_byte16(uint32_t (&c)[4], int i, uint32_t v) 
 // crosses L: missing bytes are zero (so the emitted fields equal
 // (s_i*16) mod 64 and (s_{i+1}*4) mod 64) and '=' pads are substituted.
 // FULL: the tile has exactly EncG<P>::kIn bytes (no tail / inactive-lane checks).
-template <int IA, int OA, bool FULL, int P>
+// DIRECT (FULL tiles with a 16-byte aligned destination): each thread's 16
+// chars go straight from registers to HBM with one coalesced 16-byte store
+// (512 contiguous bytes per warp instruction), no smem staging, no CTA sync.
+template <int IA, int OA, bool FULL, int P, bool DIRECT = false>
 __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *sout, int tid,
-                                            int lane) {
+                                            int lane, uint8_t *gdst = nullptr) {
+  if (B64_SKELETON) return;
 #pragma unroll
   for (int pass = 0; pass < P; ++pass) {
     const int bo = pass * (kNT * 12) + tid * 12;
@@ -239,7 +254,11 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
         if (left == 1) set_byte16(c, last + 2, '=');
       }
     }
-    store_words<OA, 4>(sout + co, c, active, lane);
+    if constexpr (DIRECT) {
+      st_global_v4(gdst + co, c);
+    } else {
+      store_words<OA, 4>(sout + co, c, active, lane);
+    }
   }
 }
 
@@ -254,11 +273,17 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
 // warp __reduce_min_sync.  Returns (lane 0 meaningful) the tile-relative
 // minimum error offset, or 0xFFFFFFFF.
 // FULL: the tile has exactly DecG<P>::kIn chars and is not a final tile.
-template <int IA, int OA, bool FULL, int P>
+// DIRECT (FULL tiles, 16-byte aligned destination): the warp stages its 384
+// output bytes of the pass in its own slice of smem (3 conflict-free STS per
+// lane), then lanes 0..23 copy them to HBM with coalesced 16-byte stores --
+// warp-local, no CTA-wide barrier, no bulk-store round trip.
+template <int IA, int OA, bool FULL, int P, bool DIRECT = false>
 __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8_t *sout,
                                                 int tid, int lane,
-                                                bool final_tile, uint32_t ch2, uint32_t ch1) {
+                                                bool final_tile, uint32_t ch2, uint32_t ch1,
+                                                uint8_t *gdst = nullptr) {
   uint32_t errmin = 0xFFFFFFFFu;
+  if (B64_SKELETON) return errmin;
   const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(g_dec_tab));
 #pragma unroll
   for (int pass = 0; pass < P; ++pass) {
@@ -319,6 +344,14 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
     o[1] = __byte_perm(V[1], V[2], 0x5601);
     o[2] = __byte_perm(V[2], V[3], 0x4560);
     store_words<(OA >= 4 ? 4 : 1), 3>(sout + bo, o, active, lane);
+    if constexpr (DIRECT) {
+      __syncwarp();
+      const int wo = pass * (kNT * 12) + (tid & ~31) * 12;  // this warp's 384-byte slice
+      if (lane < 24) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(sout + wo + 16 * lane);
+        st_global_v4(gdst + wo + 16 * lane, v);
+      }
+    }
   }
   return errmin;
 }

@@ -190,6 +190,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
     uint8_t *gdst = out + d.dst;
     const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
+    if (OA == 16 && !BATCH && d.len == G::kIn) {
+      // Full tile, aligned destination: direct coalesced stores, warp-local.
+      encode_tile<IA, OA, true, G::kPasses, true>(S.in[s] + imis, d.len, nullptr, tid, lane, gdst);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[s]);
+      continue;
+    }
     if (d.len == G::kIn)
       encode_tile<IA, OA, true, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, tid, lane);
     else
@@ -286,8 +293,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       ch2 = sin[d.len - 2];
       pads = ch1 == '=' ? (ch2 == '=' ? 2 : 1) : 0;
     }
+    const bool direct = OA == 16 && !BATCH && d.len == G::kIn && !fin;
     const uint32_t werr =
-        (d.len == G::kIn && !fin)
+        direct ? decode_tile<IA, OA, true, G::kPasses, true>(sin, d.len, S.out[so] + omis, tid, lane,
+                                                             false, 0, 0, gdst)
+        : (d.len == G::kIn && !fin)
             ? decode_tile<IA, OA, true, G::kPasses>(sin, d.len, S.out[so] + omis, tid, lane,
                                                     false, 0, 0)
             : decode_tile<IA, OA, false, G::kPasses>(sin, d.len, S.out[so] + omis, tid, lane,
@@ -305,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         __threadfence();
       }
     }
+    if (direct) continue;
     fence_proxy_async_smem();
     if (tid == 0) bulk_wait_read<kStagesOut - 2>();
     named_bar_sync(1, kNT);
@@ -345,7 +356,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   if (tid == 0) bulk_wait<0>();
 
   if constexpr (!BATCH) {
-    // Last CTA out computes the result record and resets the scratch.
+    // Last CTA out computes the result record and resets the scratch.  The
+    // barrier orders every warp's error atomics before the done count.
+    named_bar_sync(1, kNT);
     if (tid == 0) {
       __threadfence();
       const unsigned prev = atomicAdd(&ws->done, 1u);

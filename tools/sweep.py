@@ -29,6 +29,12 @@ VARIANTS = {
     "w16_c1": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1},
     "w12_c1_p4": {"B64_WARPS_C": 12, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 6},
     "p8_c1": {"B64_SINGLE_PASSES": 8, "B64_CTAS_PER_SM": 1},
+    "skel": {"B64_SKELETON": 1},
+    "skel_w16_c1": {"B64_SKELETON": 1, "B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1},
+    "w16_c1_in3": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 3},
+    "w16_c1_p2_in6": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_SINGLE_PASSES": 2, "B64_STAGES_IN": 6},
+    "w16_c1_out3": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_STAGES_OUT": 3, "B64_STAGES_IN": 3},
+    "w8_c2_p3": {"B64_SINGLE_PASSES": 3, "B64_STAGES_IN": 5},
 }
 
 
@@ -52,6 +58,8 @@ def run(names, workload, steps, reps):
         for n in names:
             lib = os.path.join(OUT, f"libb64gpu_{n}.so")
             env = dict(os.environ, B64GPU_LIB=lib)
+            if "skel" in n:
+                env["B64_BENCH_NOCHECK"] = "1"
             cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", workload, "--steps", str(steps),
                    "--warmup", "3", "--no-e2e", "--no-cpu"]
             p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
