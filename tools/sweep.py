@@ -17,8 +17,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "build", "variants")
 SRC = os.path.join(ROOT, "paper_1704_00605_b200", "csrc", "b64_lib.cu")
 
+# Before commit "w16 c1 in3": the defaults were 8 warps x 2 CTAs/SM, 4 input stages.
 VARIANTS = {
     "base": {},
+    "old_w8_c2_in4": {"B64_WARPS_C": 8, "B64_CTAS_PER_SM": 2, "B64_STAGES_IN": 4},
     "store_ef": {"B64_STORE_EVICT_FIRST": 1},
     "in3": {"B64_STAGES_IN": 3},
     "in5": {"B64_STAGES_IN": 5},
@@ -35,6 +37,14 @@ VARIANTS = {
     "w16_c1_p2_in6": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_SINGLE_PASSES": 2, "B64_STAGES_IN": 6},
     "w16_c1_out3": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_STAGES_OUT": 3, "B64_STAGES_IN": 3},
     "w8_c2_p3": {"B64_SINGLE_PASSES": 3, "B64_STAGES_IN": 5},
+    "w16_c1_in2": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 2},
+    "w16_c1_in3o2": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 3, "B64_STAGES_OUT": 2},
+    "w16_c1_p2_in4": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_SINGLE_PASSES": 2, "B64_STAGES_IN": 4},
+    "w16_c1_p3_in3": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_SINGLE_PASSES": 3, "B64_STAGES_IN": 3},
+    "w8_c2_in3": {"B64_STAGES_IN": 3},
+    "w12_c1_in3": {"B64_WARPS_C": 12, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 3},
+    "w24_c1_p2_in3": {"B64_WARPS_C": 24, "B64_CTAS_PER_SM": 1, "B64_SINGLE_PASSES": 2, "B64_STAGES_IN": 3},
+    "skel_w16_c1_in3": {"B64_SKELETON": 1, "B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 3},
 }
 
 
