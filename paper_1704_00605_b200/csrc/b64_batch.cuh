@@ -1,0 +1,427 @@
+// b64_batch.cuh -- batched encode / decode of k independent messages
+// (BASELINE.json configs[1]).
+//
+// Work is split into *units*: one unit = kBatchPasses passes of one warp
+// (encode: 768 input bytes -> 1024 chars; decode: 1024 chars -> 768 bytes).
+// A unit never straddles messages, so a message of len bytes has
+// ceil(len / unit) units (at most one partial unit per message, <= 2-4 %
+// slack at data-URI sizes).  The planner scans the message lengths once
+// (output offsets + unit offsets); every warp of the persistent grid then
+// takes an equal, contiguous range of units -- i.e. messages are assigned to
+// warps by prefix-summed lengths -- finds its first message with one 32-ary
+// search and walks forward.  Warps are fully independent: each owns a
+// 4-slot ring of 1-D TMA bulk loads (its lane 0 issues them, one mbarrier per
+// slot), a private output slice in smem, and writes its unit's output with
+// coalesced 16-byte stores (byte stores for the <16-byte unaligned edges).
+// There is no CTA-wide barrier on the hot path.
+#pragma once
+#include <climits>
+#include <cstdint>
+#include <type_traits>
+
+#include "b64_codec.cuh"
+#include "b64_ptx.cuh"
+
+namespace b64 {
+
+using namespace ptx;
+
+constexpr int kBWarps = B64_BATCH_WARPS;
+constexpr int kBSlots = B64_BATCH_SLOTS;
+constexpr int kBThreads = kBWarps * 32;
+constexpr int kFlagLast = 2;  // unit is the last unit of its message
+
+template <int P>
+struct EncUnit {
+  static constexpr int kIn = 32 * 12 * P;
+  static constexpr int kOut = 32 * 16 * P;
+};
+template <int P>
+struct DecUnit {
+  static constexpr int kIn = 32 * 16 * P;
+  static constexpr int kOut = 32 * 12 * P;
+};
+using EU = EncUnit<kBatchPasses>;
+using DU = DecUnit<kBatchPasses>;
+
+struct UnitDesc {
+  int64_t src;     // input offset of the unit (relative to d_in)
+  int64_t dst;     // output offset (relative to d_out)
+  int64_t rel;     // input offset of the unit within its message
+  int32_t len;     // input bytes of the unit (decode: multiple of 4, may be 0 < len)
+  int32_t msg;     // message index
+  int32_t flags;   // kFlagLast | kFlagFinal
+  int32_t nunits;  // units of the message
+};
+
+template <int IN, int OUT>
+struct alignas(16) WarpRing {
+  static constexpr int kInStride = round_up_c(IN + 32, 16);
+  static constexpr int kOutStride = round_up_c(OUT + 32, 16);
+  uint8_t in[kBSlots][kInStride];
+  uint8_t out[kOutStride];
+  UnitDesc desc[kBSlots];
+  uint64_t full[kBSlots];
+};
+using EncRing = WarpRing<EU::kIn, EU::kOut>;
+using DecRing = WarpRing<DU::kIn, DU::kOut>;
+
+struct BatchHeader {
+  int64_t nunits;
+  int64_t pad[3];
+};
+
+// ------------------------------------------------------------- planner ---
+// One CTA of 1024 threads, ITEMS consecutive messages per thread per round.
+// Round = (1) per-thread sums of output sizes and unit counts, (2) block
+// exclusive scan, (3) re-walk the thread's messages writing out_off,
+// unit_off and (decode) the per-message result initialisation.
+constexpr int kPlanThreads = 1024;
+constexpr int kPlanItems = 10;
+
+__device__ __forceinline__ void block_exclusive_scan2(int64_t a, int64_t b, int64_t &pa,
+                                                      int64_t &pb, int64_t &ta, int64_t &tb,
+                                                      int64_t *sh /* 66 */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t xa = __shfl_up_sync(0xffffffffu, ia, o);
+    const int64_t xb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) {
+      ia += xa;
+      ib += xb;
+    }
+  }
+  if (lane == 31) {
+    sh[warp] = ia;
+    sh[32 + warp] = ib;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t wa = sh[lane], wb = sh[32 + lane];
+    int64_t sa = wa, sb = wb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t xa = __shfl_up_sync(0xffffffffu, sa, o);
+      const int64_t xb = __shfl_up_sync(0xffffffffu, sb, o);
+      if (lane >= o) {
+        sa += xa;
+        sb += xb;
+      }
+    }
+    sh[lane] = sa - wa;
+    sh[32 + lane] = sb - wb;
+    if (lane == 31) {
+      sh[64] = sa;
+      sh[65] = sb;
+    }
+  }
+  __syncthreads();
+  pa = sh[warp] + ia - a;
+  pb = sh[32 + warp] + ib - b;
+  ta = sh[64];
+  tb = sh[65];
+  __syncthreads();
+}
+
+// Output size and unit count of message [a, b) (decode: reads the pads).
+template <bool DECODE>
+__device__ __forceinline__ void msg_sizes(const uint8_t *in, int64_t a, int64_t b, int64_t &osz,
+                                          int64_t &units) {
+  const int64_t len = b - a;
+  if (DECODE) {
+    const int64_t q = len / 4;
+    int64_t p = 0;
+    if ((len & 3) == 0 && q > 0 && in[b - 1] == '=') p = (in[b - 2] == '=') ? 2 : 1;
+    osz = 3 * q - p;
+    units = (4 * q + DU::kIn - 1) / DU::kIn;
+  } else {
+    osz = 4 * ((len + 2) / 3);
+    units = (len + EU::kIn - 1) / EU::kIn;
+  }
+}
+
+template <bool DECODE>
+__global__ void __launch_bounds__(kPlanThreads)
+    plan_kernel(const uint8_t *__restrict__ in, const int64_t *__restrict__ in_off, int64_t k,
+                int64_t *__restrict__ out_off, int64_t *__restrict__ unit_off, BatchHeader *hdr,
+                int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
+                int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
+  __shared__ int64_t sh[66];
+  int64_t carry_o = 0, carry_u = 0;
+  for (int64_t base = 0; base < k; base += static_cast<int64_t>(kPlanThreads) * kPlanItems) {
+    const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * kPlanItems;
+    const int nit = static_cast<int>(i0 >= k ? 0 : (k - i0 < kPlanItems ? k - i0 : kPlanItems));
+    int64_t so = 0, su = 0;
+    for (int t = 0; t < nit; ++t) {
+      int64_t o, u;
+      msg_sizes<DECODE>(in, in_off[i0 + t], in_off[i0 + t + 1], o, u);
+      so += o;
+      su += u;
+    }
+    int64_t po, pu, to, tu;
+    block_exclusive_scan2(so, su, po, pu, to, tu, sh);
+    int64_t ro = carry_o + po, ru = carry_u + pu;
+    for (int t = 0; t < nit; ++t) {
+      const int64_t i = i0 + t;
+      const int64_t a = in_off[i], b = in_off[i + 1];
+      int64_t o, u;
+      msg_sizes<DECODE>(in, a, b, o, u);
+      out_off[i] = ro;
+      unit_off[i] = ru;
+      if (DECODE) {
+        msg_done[i] = 0;
+        const int64_t len = b - a;
+        if (u == 0) {  // no complete quad: the result is decided here
+          status[i] = (len & 3) ? B64_ERR_LENGTH : B64_OK;
+          err_pos[i] = (len & 3) ? 0 : -1;
+          out_len[i] = 0;
+        } else {
+          err_pos[i] = LLONG_MAX;
+        }
+      }
+      ro += o;
+      ru += u;
+    }
+    carry_o += to;
+    carry_u += tu;
+  }
+  if (threadIdx.x == 0) {
+    out_off[k] = carry_o;
+    unit_off[k] = carry_u;
+    hdr->nunits = carry_u;
+  }
+}
+
+// ------------------------------------------------------ warp walker ---
+// Metadata of a window of 32 messages [base, base+32) lives in the lanes
+// (lane l holds in_off/out_off/unit_off of message base+l); message j in
+// [base, base+31) is then fully described by lanes j-base and j-base+1.
+struct MsgWindow {
+  int64_t base = -1;
+  int64_t io, oo, uo;  // this lane's entries
+};
+
+__device__ __forceinline__ void window_load(MsgWindow &w, int64_t base, int64_t k,
+                                            const int64_t *in_off, const int64_t *out_off,
+                                            const int64_t *unit_off, int lane) {
+  w.base = base;
+  const int64_t j = base + lane;
+  const bool ok = j <= k;
+  w.io = ok ? in_off[j] : 0;
+  w.oo = ok ? out_off[j] : 0;
+  w.uo = ok ? unit_off[j] : 0;
+}
+
+// Largest i in [0, k) with unit_off[i] <= u (unit_off[k] > u): the message
+// holding unit u.  32-ary search, one coalesced probe per round.
+__device__ __forceinline__ int64_t find_message(const int64_t *unit_off, int64_t k, int64_t u,
+                                                int lane) {
+  int64_t lo = 0, hi = k;  // invariant: unit_off[lo] <= u < unit_off[hi]
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + static_cast<int64_t>(lane) * step;
+    const bool le = p < hi && unit_off[p] <= u;
+    const unsigned mask = __ballot_sync(0xffffffffu, le);
+    const int L = 31 - __clz(mask);  // lane 0 always true (p = lo)
+    const int64_t nlo = lo + static_cast<int64_t>(L) * step;
+    const int64_t nhi = nlo + step < hi ? nlo + step : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
+// Unit-level copy-out: `len` bytes staged at sbuf (same address mod 16 as
+// gdst) -> gdst: interior 16-byte granules by the lanes, edges byte-wise.
+__device__ __forceinline__ void warp_copy_out(uint8_t *gdst, const uint8_t *sbuf, int len,
+                                              int lane) {
+  const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
+  const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
+  const uintptr_t a1 = (g + static_cast<uintptr_t>(len)) & ~static_cast<uintptr_t>(15);
+  if (a1 > a0) {
+    const int head = static_cast<int>(a0 - g);
+    const int ng = static_cast<int>((a1 - a0) >> 4);
+    for (int q = lane; q < ng; q += 32) {
+      const uint4 v = *reinterpret_cast<const uint4 *>(sbuf + head + 16 * q);
+      *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a0) + 16 * q) = v;
+    }
+    const int tail0 = static_cast<int>(a1 - g);
+    if (lane < head) gdst[lane] = sbuf[lane];
+    if (lane >= 16 && lane - 16 < len - tail0) gdst[tail0 + lane - 16] = sbuf[tail0 + lane - 16];
+  } else {
+    if (lane < len) gdst[lane] = sbuf[lane];
+  }
+}
+
+// --------------------------------------------------------- the kernel ---
+template <bool DECODE>
+__global__ void __launch_bounds__(kBThreads, 1)
+    batch_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t k,
+                 const int64_t *__restrict__ in_off, const int64_t *__restrict__ out_off,
+                 const int64_t *__restrict__ unit_off, const BatchHeader *__restrict__ hdr,
+                 int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
+                 int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
+  using Ring = typename std::conditional<DECODE, DecRing, EncRing>::type;
+  constexpr int UIN = DECODE ? DU::kIn : EU::kIn;
+  constexpr int UOUT = DECODE ? DU::kOut : EU::kOut;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  Ring &R = reinterpret_cast<Ring *>(smem_raw)[warp];
+
+  if (DECODE) {
+    if (tid < 256) g_dec_tab[tid] = kInvalid;
+    __syncthreads();
+    if (tid < 64) g_dec_tab[ascii_of(tid)] = static_cast<uint8_t>(tid);
+  } else {
+    if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid));
+  }
+  if (lane == 0) {
+    for (int s = 0; s < kBSlots; ++s) mbar_init(&R.full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int64_t U = hdr->nunits;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kBWarps + warp;
+  const int64_t GW = static_cast<int64_t>(gridDim.x) * kBWarps;
+  const int64_t u_begin = static_cast<int64_t>((static_cast<__int128>(U) * gw) / GW);
+  const int64_t u_end = static_cast<int64_t>((static_cast<__int128>(U) * (gw + 1)) / GW);
+  if (u_begin >= u_end) return;
+
+  const uint64_t pol = policy_evict_first();
+  // ---- issue-side walker state
+  MsgWindow win;
+  int64_t msg = find_message(unit_off, k, u_begin, lane);
+  window_load(win, msg, k, in_off, out_off, unit_off, lane);
+  auto field = [&](int64_t v, int64_t j) { return __shfl_sync(0xffffffffu, v, static_cast<int>(j - win.base)); };
+  int64_t m_in = field(win.io, msg), m_end = field(win.io, msg + 1);
+  int64_t m_out = field(win.oo, msg), m_u0 = field(win.uo, msg), m_u1 = field(win.uo, msg + 1);
+
+  auto issue = [&](int64_t u) {
+    while (u >= m_u1) {  // advance to the message holding unit u (skips empty messages)
+      ++msg;
+      if (msg + 1 >= win.base + 32) window_load(win, msg, k, in_off, out_off, unit_off, lane);
+      m_in = field(win.io, msg);
+      m_end = field(win.io, msg + 1);
+      m_out = field(win.oo, msg);
+      m_u0 = field(win.uo, msg);
+      m_u1 = field(win.uo, msg + 1);
+    }
+    const int64_t r = u - m_u0;
+    const int64_t mlen = m_end - m_in;
+    const int64_t eff = DECODE ? 4 * (mlen / 4) : mlen;
+    UnitDesc d;
+    d.rel = r * UIN;
+    d.src = m_in + d.rel;
+    d.dst = m_out + r * UOUT;
+    const int64_t left = eff - d.rel;
+    d.len = static_cast<int32_t>(left < UIN ? left : UIN);
+    d.msg = static_cast<int32_t>(msg);
+    d.nunits = static_cast<int32_t>(m_u1 - m_u0);
+    const bool last = u == m_u1 - 1;
+    d.flags = (last ? kFlagLast : 0) | ((DECODE && last && (mlen & 3) == 0) ? kFlagFinal : 0);
+    if (lane == 0) {
+      const int s = static_cast<int>((u - u_begin) % kBSlots);
+      R.desc[s] = d;
+      const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
+      const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
+      const uintptr_t g1 = (g + static_cast<uintptr_t>(d.len) + 15) & ~static_cast<uintptr_t>(15);
+      const uint32_t bytes = static_cast<uint32_t>(g1 - g0);
+      mbar_arrive_expect_tx(&R.full[s], bytes);
+      bulk_g2s(R.in[s], reinterpret_cast<const void *>(g0), bytes, &R.full[s], pol);
+    }
+  };
+
+  int64_t iu = u_begin;
+  for (; iu < u_end && iu < u_begin + kBSlots; ++iu) issue(iu);
+
+  for (int64_t cu = u_begin; cu < u_end; ++cu) {
+    const int64_t it = cu - u_begin;
+    const int s = static_cast<int>(it % kBSlots);
+    mbar_wait_spin(&R.full[s], static_cast<uint32_t>((it / kBSlots) & 1));
+    const UnitDesc d = R.desc[s];
+    const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
+    const uint8_t *sin = R.in[s] + imis;
+    uint8_t *gdst = out + d.dst;
+    const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
+    uint8_t *sout = R.out + omis;
+    int olen;
+    uint32_t werr = 0xFFFFFFFFu;
+    if constexpr (!DECODE) {
+      if (d.len == UIN)
+        encode_tile<1, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+      else
+        encode_tile<1, 1, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+      olen = 4 * ((d.len + 2) / 3);
+    } else {
+      const bool fin = (d.flags & kFlagFinal) != 0;
+      uint32_t ch1 = 0, ch2 = 0;
+      int pads = 0;
+      if (fin) {
+        ch1 = sin[d.len - 1];
+        ch2 = sin[d.len - 2];
+        pads = ch1 == '=' ? (ch2 == '=' ? 2 : 1) : 0;
+      }
+      werr = (d.len == UIN && !fin)
+                 ? decode_tile<1, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
+                                                                     false, 0, 0)
+                 : decode_tile<1, 1, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
+                                                                      fin, ch2, ch1);
+      olen = 3 * (d.len / 4) - pads;
+    }
+    __syncwarp();
+    // Slot s is fully read: order those generic reads before the next bulk
+    // write into it, then refill the ring.
+    fence_proxy_async_smem();
+    if (iu < u_end) {
+      issue(iu);
+      ++iu;
+    }
+    warp_copy_out(gdst, R.out + omis, olen, lane);
+    if constexpr (DECODE) {
+      if (lane == 0) {
+        if (werr != 0xFFFFFFFFu) {
+          unsigned long long *tgt = reinterpret_cast<unsigned long long *>(err_pos + d.msg);
+          const unsigned long long pos = static_cast<unsigned long long>(d.rel) + werr;
+          if (pos < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, pos);
+        }
+        // Per-message completion: the warp finishing the message's last
+        // unit writes its result (status is a pure function of err_pos).
+        bool mine = d.nunits == 1;
+        if (!mine) {
+          __threadfence();
+          mine = atomicAdd(msg_done + d.msg, 1u) == static_cast<unsigned>(d.nunits - 1);
+        }
+        if (mine) {
+          __threadfence();
+          const int64_t i = d.msg;
+          const int64_t len = in_off[i + 1] - in_off[i];
+          const int64_t q = len / 4, r = len % 4;
+          const int64_t cap = out_off[i + 1] - out_off[i];
+          const unsigned long long e =
+              d.nunits == 1 ? (werr != 0xFFFFFFFFu ? static_cast<unsigned long long>(d.rel) + werr
+                                                   : static_cast<unsigned long long>(LLONG_MAX))
+                            : atomicOr(reinterpret_cast<unsigned long long *>(err_pos + i), 0ull);
+          int64_t err = e == static_cast<unsigned long long>(LLONG_MAX) ? -1 : static_cast<int64_t>(e);
+          if (err < 0 && r != 0) err = 4 * q;
+          if (err < 0) {
+            status[i] = B64_OK;
+            out_len[i] = cap;
+          } else if (r != 0 && err == 4 * q) {
+            status[i] = B64_ERR_LENGTH;
+            out_len[i] = 3 * q;
+          } else {
+            status[i] = B64_ERR_INVALID_CHAR;
+            out_len[i] = 3 * (err / 4);
+          }
+          err_pos[i] = err;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace b64

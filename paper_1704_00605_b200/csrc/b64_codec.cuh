@@ -22,8 +22,14 @@ namespace b64 {
 #ifndef B64_SINGLE_PASSES
 #define B64_SINGLE_PASSES 4
 #endif
-#ifndef B64_BATCH_PASSES
-#define B64_BATCH_PASSES 1
+#ifndef B64_BATCH_PASSES  // passes of one warp per batched work unit
+#define B64_BATCH_PASSES 2
+#endif
+#ifndef B64_BATCH_SLOTS   // per-warp input ring depth (batched)
+#define B64_BATCH_SLOTS 4
+#endif
+#ifndef B64_BATCH_WARPS   // warps per CTA (batched)
+#define B64_BATCH_WARPS 16
 #endif
 #ifndef B64_CTAS_PER_SM
 #define B64_CTAS_PER_SM 1
@@ -58,7 +64,7 @@ struct DecG {
   static constexpr int kOut = kNT * 12 * P;  // output bytes per tile
 };
 constexpr int kSinglePasses = B64_SINGLE_PASSES;  // single buffer: 12 KiB in / 16 KiB out (encode)
-constexpr int kBatchPasses = B64_BATCH_PASSES;    // batched: small tiles for data-URI-sized messages
+constexpr int kBatchPasses = B64_BATCH_PASSES;    // batched: one warp unit = this many passes
 
 constexpr int round_up_c(int x, int a) { return (x + a - 1) / a * a; }
 
@@ -222,13 +228,13 @@ __device__ __forceinline__ void set_byte16(uint32_t (&c)[4], int i, uint32_t v) 
 // DIRECT (FULL tiles with a 16-byte aligned destination): each thread's 16
 // chars go straight from registers to HBM with one coalesced 16-byte store
 // (512 contiguous bytes per warp instruction), no smem staging, no CTA sync.
-template <int IA, int OA, bool FULL, int P, bool DIRECT = false>
+template <int IA, int OA, bool FULL, int P, bool DIRECT = false, int NT = kNT>
 __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *sout, int tid,
                                             int lane, uint8_t *gdst = nullptr) {
 #pragma unroll
   for (int pass = 0; pass < P; ++pass) {
-    const int bo = pass * (kNT * 12) + tid * 12;
-    const int co = pass * (kNT * 16) + tid * 16;
+    const int bo = pass * (NT * 12) + tid * 12;
+    const int co = pass * (NT * 16) + tid * 16;
     const bool active = FULL || bo < L;
     if (!FULL && !__any_sync(0xffffffffu, active)) break;
     uint32_t w[3];
@@ -280,7 +286,7 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
 // output bytes of the pass in its own slice of smem (3 conflict-free STS per
 // lane), then lanes 0..23 copy them to HBM with coalesced 16-byte stores --
 // warp-local, no CTA-wide barrier, no bulk-store round trip.
-template <int IA, int OA, bool FULL, int P, bool DIRECT = false>
+template <int IA, int OA, bool FULL, int P, bool DIRECT = false, int NT = kNT>
 __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8_t *sout,
                                                 int tid, int lane,
                                                 bool final_tile, uint32_t ch2, uint32_t ch1,
@@ -289,8 +295,8 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
   const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(g_dec_tab));
 #pragma unroll
   for (int pass = 0; pass < P; ++pass) {
-    const int co = pass * (kNT * 16) + tid * 16;
-    const int bo = pass * (kNT * 12) + tid * 12;
+    const int co = pass * (NT * 16) + tid * 16;
+    const int bo = pass * (NT * 12) + tid * 12;
     const bool active = FULL || co < L;
     if (!FULL && !__any_sync(0xffffffffu, active)) break;
     uint32_t w[4];
@@ -306,7 +312,7 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
       store_words<(OA >= 4 ? 4 : 1), 3>(sout + bo, o, active, lane);
       if constexpr (DIRECT) {
         __syncwarp();
-        const int wo = pass * (kNT * 12) + (tid & ~31) * 12;
+        const int wo = pass * (NT * 12) + (tid & ~31) * 12;
         if (lane < 24) {
           const uint4 q = *reinterpret_cast<const uint4 *>(sout + wo + 16 * lane);
           st_global_v4(gdst + wo + 16 * lane, q);
@@ -361,7 +367,7 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
     store_words<(OA >= 4 ? 4 : 1), 3>(sout + bo, o, active, lane);
     if constexpr (DIRECT) {
       __syncwarp();
-      const int wo = pass * (kNT * 12) + (tid & ~31) * 12;  // this warp's 384-byte slice
+      const int wo = pass * (NT * 12) + (tid & ~31) * 12;  // this warp's 384-byte slice
       if (lane < 24) {
         const uint4 v = *reinterpret_cast<const uint4 *>(sout + wo + 16 * lane);
         st_global_v4(gdst + wo + 16 * lane, v);

@@ -14,12 +14,14 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <type_traits>
 #include <mutex>
 #include <utility>
 
 #include "../../include/b64gpu.h"
 #include "b64_codec.cuh"
 #include "b64_ptx.cuh"
+#include "b64_batch.cuh"
 
 namespace b64 {
 
@@ -36,16 +38,10 @@ struct alignas(128) Smem {
   uint64_t full[kStagesIn];
   uint64_t empty[kStagesIn];
 };
-template <bool BATCH>
-using EncGeo = EncG<BATCH ? kBatchPasses : kSinglePasses>;
-template <bool BATCH>
-using DecGeo = DecG<BATCH ? kBatchPasses : kSinglePasses>;
-template <bool BATCH>
-using EncSmem = Smem<EncGeo<BATCH>::kIn, EncGeo<BATCH>::kOut>;
-template <bool BATCH>
-using DecSmem = Smem<DecGeo<BATCH>::kIn, DecGeo<BATCH>::kOut>;
-using EncS1 = EncGeo<false>;  // single-buffer tile geometry
-using DecS1 = DecGeo<false>;
+using EncS1 = EncG<kSinglePasses>;  // single-buffer tile geometry
+using DecS1 = DecG<kSinglePasses>;
+using EncSmem = Smem<EncS1::kIn, EncS1::kOut>;
+using DecSmem = Smem<DecS1::kIn, DecS1::kOut>;
 
 struct DecWs {                 // per-(device, stream) decode scratch (self-resetting)
   unsigned long long errkey;   // min error offset, ~0 = none
@@ -84,48 +80,25 @@ __device__ __forceinline__ TileDesc dec_single_desc(int64_t j, int64_t ntiles, i
 // --------------------------------------------------- producer warp ---
 // Lane 0 owns the ring: wait for the slot, publish the descriptor, arm the
 // full barrier with the byte count and issue the bulk copy of the tile's
-// 16-byte aligned window.  Batched descriptors are fetched 32 at a time by
-// the whole warp and handed to lane 0 by shuffles.
-template <bool BATCH, bool DECODE, class SmemT>
+// 16-byte aligned window (evict-first: the input is streamed once).
+template <bool DECODE, class SmemT>
 __device__ __forceinline__ void producer_loop(SmemT &S, const uint8_t *in, int64_t ntiles,
-                                              int64_t n_or_chars, bool final_pad_rules,
-                                              const TileDesc *descs, int lane) {
+                                              int64_t n_or_chars, bool final_pad_rules, int lane) {
+  if (lane != 0) return;
   const uint64_t pol = policy_evict_first();
   int it = 0;
-  TileDesc mine;
   for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
-    TileDesc d;
-    if constexpr (BATCH) {
-      if ((it & 31) == 0) {
-        const int64_t jj = j + static_cast<int64_t>(lane) * gridDim.x;
-        if (jj < ntiles) mine = descs[jj];
-      }
-      const int src_lane = it & 31;
-      d.src = __shfl_sync(0xffffffffu, mine.src, src_lane);
-      d.dst = __shfl_sync(0xffffffffu, mine.dst, src_lane);
-      d.rel = __shfl_sync(0xffffffffu, mine.rel, src_lane);
-      d.len = __shfl_sync(0xffffffffu, mine.len, src_lane);
-      d.msg = __shfl_sync(0xffffffffu, mine.msg, src_lane);
-      d.flags = __shfl_sync(0xffffffffu, mine.flags, src_lane);
-      d.ntiles = __shfl_sync(0xffffffffu, mine.ntiles, src_lane);
-    } else {
-      if constexpr (DECODE) {
-        d = dec_single_desc(j, ntiles, n_or_chars, final_pad_rules);
-      } else {
-        d = enc_single_desc(j, n_or_chars);
-      }
-    }
-    if (lane == 0) {
-      const int s = it % kStagesIn;
-      if (it >= kStagesIn) mbar_wait(&S.empty[s], ((it / kStagesIn) & 1) ^ 1);
-      S.desc[s] = d;
-      const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
-      const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
-      const uintptr_t g1 = (g + static_cast<uintptr_t>(d.len) + 15) & ~static_cast<uintptr_t>(15);
-      const uint32_t bytes = static_cast<uint32_t>(g1 - g0);
-      mbar_arrive_expect_tx(&S.full[s], bytes);
-      bulk_g2s(S.in[s], reinterpret_cast<const void *>(g0), bytes, &S.full[s], pol);
-    }
+    const TileDesc d = DECODE ? dec_single_desc(j, ntiles, n_or_chars, final_pad_rules)
+                              : enc_single_desc(j, n_or_chars);
+    const int s = it % kStagesIn;
+    if (it >= kStagesIn) mbar_wait(&S.empty[s], ((it / kStagesIn) & 1) ^ 1);
+    S.desc[s] = d;
+    const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
+    const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
+    const uintptr_t g1 = (g + static_cast<uintptr_t>(d.len) + 15) & ~static_cast<uintptr_t>(15);
+    const uint32_t bytes = static_cast<uint32_t>(g1 - g0);
+    mbar_arrive_expect_tx(&S.full[s], bytes);
+    bulk_g2s(S.in[s], reinterpret_cast<const void *>(g0), bytes, &S.full[s], pol);
   }
 }
 
@@ -156,16 +129,16 @@ __device__ __forceinline__ void copy_out(uint8_t *gdst, const uint8_t *sbuf, int
 }
 
 // ------------------------------------------------------ encode kernel ---
-template <int IA, int OA, bool BATCH>
+// Single buffer (rows a1-a5).  IA / OA: guaranteed alignment class of the
+// input / output pointer (16, 4 or 1).
+template <int IA, int OA>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     encode_kernel(const uint8_t *__restrict__ in, int64_t n, uint8_t *__restrict__ out,
-                  int64_t ntiles_arg, const TileDesc *__restrict__ descs,
-                  const int64_t *__restrict__ ntiles_dev) {
+                  int64_t ntiles) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using G = EncGeo<BATCH>;
-  EncSmem<BATCH> &S = *reinterpret_cast<EncSmem<BATCH> *>(smem_raw);
+  using G = EncS1;
+  EncSmem &S = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t ntiles = BATCH ? *ntiles_dev : ntiles_arg;
   if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid));  // Table I / II
   if (tid == 0) {
     for (int s = 0; s < kStagesIn; ++s) {
@@ -177,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   __syncthreads();
 
   if (warp == kWarpsC) {
-    producer_loop<BATCH, false>(S, in, ntiles, n, false, descs, lane);
+    producer_loop<false>(S, in, ntiles, n, false, lane);
     return;
   }
 
@@ -190,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
     uint8_t *gdst = out + d.dst;
     const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
-    if (OA == 16 && !BATCH && d.len == G::kIn) {
+    if (OA == 16 && d.len == G::kIn) {
       // Full tile, aligned destination: direct coalesced stores, warp-local.
       encode_tile<IA, OA, true, G::kPasses, true>(S.in[s] + imis, d.len, nullptr, tid, lane, gdst);
       __syncwarp();
@@ -241,20 +214,16 @@ __device__ void finalize_single(const uint8_t *in, int64_t m, bool final_shard,
   res->pad_count = p;
 }
 
-template <int IA, int OA, bool BATCH>
+// Single buffer / shard (rows a6-a12).
+template <int IA, int OA>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
-                  int64_t ntiles_arg, int final_shard, DecWs *ws, b64_result *res,
-                  const TileDesc *__restrict__ descs, const int64_t *__restrict__ ntiles_dev,
-                  const int64_t *__restrict__ in_off, const int64_t *__restrict__ out_off,
-                  int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
-                  int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
+                  int64_t ntiles, int final_shard, DecWs *ws, b64_result *res) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using G = DecGeo<BATCH>;
-  DecSmem<BATCH> &S = *reinterpret_cast<DecSmem<BATCH> *>(smem_raw);
+  using G = DecS1;
+  DecSmem &S = *reinterpret_cast<DecSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t ntiles = BATCH ? *ntiles_dev : ntiles_arg;
-  const int64_t chars = BATCH ? 0 : 4 * (m / 4);
+  const int64_t chars = 4 * (m / 4);
   const bool pad_rules = final_shard != 0 && (m % 4) == 0;
 
   // Inverse map A: invalid everywhere, then A(B(v)) = v.
@@ -271,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   __syncthreads();
 
   if (warp == kWarpsC) {
-    producer_loop<BATCH, true>(S, in, ntiles, chars, pad_rules, descs, lane);
+    producer_loop<true>(S, in, ntiles, chars, pad_rules, lane);
     return;
   }
 
@@ -293,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       ch2 = sin[d.len - 2];
       pads = ch1 == '=' ? (ch2 == '=' ? 2 : 1) : 0;
     }
-    const bool direct = OA == 16 && !BATCH && d.len == G::kIn && !fin;
+    const bool direct = OA == 16 && d.len == G::kIn && !fin;
     const uint32_t werr =
         direct ? decode_tile<IA, OA, true, G::kPasses, true>(sin, d.len, S.out[so] + omis, tid, lane,
                                                              false, 0, 0, gdst)
@@ -309,8 +278,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         // First-error reduction: one 64-bit atomicMin per warp,
         // skipped when a smaller offset is already recorded.
         const unsigned long long pos = static_cast<unsigned long long>(d.rel) + werr;
-        unsigned long long *tgt =
-            BATCH ? reinterpret_cast<unsigned long long *>(err_pos + d.msg) : &ws->errkey;
+        unsigned long long *tgt = &ws->errkey;
         if (pos < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, pos);
         __threadfence();
       }
@@ -321,224 +289,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     named_bar_sync(1, kNT);
     const int olen = 3 * (d.len / 4) - pads;
     copy_out(gdst, S.out[so] + omis, olen, tid, pol_out);
-    if constexpr (BATCH) {
-      // Per-message completion: the CTA finishing the message's last tile
-      // writes its result (status is a pure function of err_pos).
-      if (tid == 0) {
-        __threadfence();
-        const unsigned prev = atomicAdd(msg_done + d.msg, 1u);
-        if (prev == static_cast<unsigned>(d.ntiles - 1)) {
-          __threadfence();
-          const int64_t i = d.msg;
-          const int64_t len = in_off[i + 1] - in_off[i];
-          const int64_t q = len / 4, r = len % 4;
-          const int64_t cap = out_off[i + 1] - out_off[i];
-          const unsigned long long e =
-              atomicOr(reinterpret_cast<unsigned long long *>(err_pos + i), 0ull);
-          int64_t err = e == static_cast<unsigned long long>(LLONG_MAX) ? -1
-                                                                         : static_cast<int64_t>(e);
-          if (err < 0 && r != 0) err = 4 * q;
-          if (err < 0) {
-            status[i] = B64_OK;
-            out_len[i] = cap;
-          } else if (r != 0 && err == 4 * q) {
-            status[i] = B64_ERR_LENGTH;
-            out_len[i] = 3 * q;
-          } else {
-            status[i] = B64_ERR_INVALID_CHAR;
-            out_len[i] = 3 * (err / 4);
-          }
-          err_pos[i] = err;
-        }
-      }
-    }
   }
   if (tid == 0) bulk_wait<0>();
 
-  if constexpr (!BATCH) {
-    // Last CTA out computes the result record and resets the scratch.  The
-    // barrier orders every warp's error atomics before the done count.
-    named_bar_sync(1, kNT);
-    if (tid == 0) {
+  // Last CTA out computes the result record and resets the scratch.  The
+  // barrier orders every warp's error atomics before the done count.
+  named_bar_sync(1, kNT);
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&ws->done, 1u);
+    if (prev == gridDim.x - 1) {
       __threadfence();
-      const unsigned prev = atomicAdd(&ws->done, 1u);
-      if (prev == gridDim.x - 1) {
-        __threadfence();
-        const unsigned long long e = atomicOr(&ws->errkey, 0ull);
-        finalize_single(in, m, final_shard != 0, e, res);
-        ws->errkey = ~0ull;
-        ws->done = 0;
-        __threadfence_system();
-      }
+      const unsigned long long e = atomicOr(&ws->errkey, 0ull);
+      finalize_single(in, m, final_shard != 0, e, res);
+      ws->errkey = ~0ull;
+      ws->done = 0;
+      __threadfence_system();
     }
-  }
-}
-
-// ------------------------------------------------------ batch planner ---
-// One CTA: exclusive scans of per-message output sizes and tile counts,
-// then the tile descriptors (messages -> tiles by prefix-summed lengths).
-constexpr int kPlanThreads = 1024;
-constexpr int kPlanItems = 8;
-
-struct PlanHeader {
-  int64_t ntiles;
-  int64_t capacity;  // descriptors that fit in the workspace
-  int64_t overflow;  // 1 if capacity was exceeded (nothing is processed)
-  int64_t pad;
-};
-
-__device__ __forceinline__ void block_exclusive_scan2(int64_t a, int64_t b, int64_t &pa,
-                                                      int64_t &pb, int64_t &ta, int64_t &tb,
-                                                      int64_t *sh /* 2*32 + 2 */) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t ia = a, ib = b;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t xa = __shfl_up_sync(0xffffffffu, ia, o);
-    const int64_t xb = __shfl_up_sync(0xffffffffu, ib, o);
-    if (lane >= o) {
-      ia += xa;
-      ib += xb;
-    }
-  }
-  if (lane == 31) {
-    sh[warp] = ia;
-    sh[32 + warp] = ib;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    int64_t wa = sh[lane], wb = sh[32 + lane];
-    int64_t sa = wa, sb = wb;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t xa = __shfl_up_sync(0xffffffffu, sa, o);
-      const int64_t xb = __shfl_up_sync(0xffffffffu, sb, o);
-      if (lane >= o) {
-        sa += xa;
-        sb += xb;
-      }
-    }
-    sh[lane] = sa - wa;  // exclusive warp prefix
-    sh[32 + lane] = sb - wb;
-    if (lane == 31) {
-      sh[64] = sa;
-      sh[65] = sb;
-    }
-  }
-  __syncthreads();
-  pa = sh[warp] + ia - a;
-  pb = sh[32 + warp] + ib - b;
-  ta = sh[64];
-  tb = sh[65];
-  __syncthreads();
-}
-
-template <bool DECODE>
-__global__ void __launch_bounds__(kPlanThreads)
-    plan_kernel(const uint8_t *__restrict__ in, const int64_t *__restrict__ in_off, int64_t k,
-                int64_t *__restrict__ out_off, PlanHeader *hdr, TileDesc *__restrict__ descs,
-                int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
-                int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
-  __shared__ int64_t sh[66];
-  const int64_t cap = hdr->capacity;
-  constexpr int TILE = DECODE ? DecGeo<true>::kIn : EncGeo<true>::kIn;
-  int64_t carry_out = 0, carry_tiles = 0;
-  for (int64_t base = 0; base < k; base += static_cast<int64_t>(kPlanThreads) * kPlanItems) {
-    const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * kPlanItems;
-    int64_t len[kPlanItems], osz[kPlanItems];
-    int32_t nt[kPlanItems];
-    int64_t sum_o = 0, sum_t = 0;
-#pragma unroll
-    for (int t = 0; t < kPlanItems; ++t) {
-      const int64_t i = i0 + t;
-      len[t] = 0;
-      osz[t] = 0;
-      nt[t] = 0;
-      if (i < k) {
-        const int64_t a = in_off[i], b = in_off[i + 1];
-        len[t] = b - a;
-        if (DECODE) {
-          const int64_t q = len[t] / 4;
-          int64_t p = 0;
-          if (len[t] % 4 == 0 && q > 0 && in[b - 1] == '=') p = (in[b - 2] == '=') ? 2 : 1;
-          osz[t] = 3 * q - p;
-          nt[t] = static_cast<int32_t>((4 * q + TILE - 1) / TILE);
-        } else {
-          osz[t] = 4 * ((len[t] + 2) / 3);
-          nt[t] = static_cast<int32_t>((len[t] + TILE - 1) / TILE);
-        }
-      }
-      sum_o += osz[t];
-      sum_t += nt[t];
-    }
-    int64_t po, pt, to, tt;
-    block_exclusive_scan2(sum_o, sum_t, po, pt, to, tt, sh);
-    int64_t run_o = carry_out + po, run_t = carry_tiles + pt;
-#pragma unroll
-    for (int t = 0; t < kPlanItems; ++t) {
-      const int64_t i = i0 + t;
-      if (i < k) {
-        out_off[i] = run_o;
-        const int64_t src0 = in_off[i];
-        if (DECODE) {
-          msg_done[i] = 0;
-          const int64_t q = len[t] / 4, r = len[t] % 4;
-          if (nt[t] == 0) {  // no complete quad: decided here
-            if (r == 0) {
-              status[i] = B64_OK;
-              err_pos[i] = -1;
-            } else {
-              status[i] = B64_ERR_LENGTH;
-              err_pos[i] = 0;
-            }
-            out_len[i] = 0;
-          } else {
-            err_pos[i] = LLONG_MAX;
-          }
-          for (int32_t u = 0; u < nt[t]; ++u) {
-            const int64_t tix = run_t + u;
-            if (tix < cap) {
-              TileDesc d;
-              d.rel = static_cast<int64_t>(u) * TILE;
-              d.src = src0 + d.rel;
-              d.dst = run_o + static_cast<int64_t>(u) * (TILE / 4 * 3);
-              const int64_t left = 4 * q - d.rel;
-              d.len = static_cast<int32_t>(left < TILE ? left : TILE);
-              d.msg = static_cast<int32_t>(i);
-              d.flags = (u == nt[t] - 1 && r == 0) ? kFlagFinal : 0;
-              d.ntiles = nt[t];
-              descs[tix] = d;
-            }
-          }
-        } else {
-          for (int32_t u = 0; u < nt[t]; ++u) {
-            const int64_t tix = run_t + u;
-            if (tix < cap) {
-              TileDesc d;
-              d.rel = static_cast<int64_t>(u) * TILE;
-              d.src = src0 + d.rel;
-              d.dst = run_o + static_cast<int64_t>(u) * (TILE / 3 * 4);
-              const int64_t left = len[t] - d.rel;
-              d.len = static_cast<int32_t>(left < TILE ? left : TILE);
-              d.msg = static_cast<int32_t>(i);
-              d.flags = 0;
-              d.ntiles = nt[t];
-              descs[tix] = d;
-            }
-          }
-        }
-      }
-      run_o += osz[t];
-      run_t += nt[t];
-    }
-    carry_out += to;
-    carry_tiles += tt;
-  }
-  if (threadIdx.x == 0) {
-    out_off[k] = carry_out;
-    const bool ovf = carry_tiles > cap;
-    hdr->overflow = ovf ? 1 : 0;
-    hdr->ntiles = ovf ? 0 : carry_tiles;
   }
 }
 
@@ -574,22 +341,21 @@ cudaError_t set_smem(K kernel, int bytes) {
 }
 
 // Kernel tables indexed by alignment class (0: 16-aligned, 1: 4-aligned, 2: unaligned).
-using EncFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, const TileDesc *,
-                       const int64_t *);
-using DecFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int, DecWs *, b64_result *,
-                       const TileDesc *, const int64_t *, const int64_t *, const int64_t *,
-                       int64_t *, int64_t *, int32_t *, unsigned int *);
+using EncFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t);
+using DecFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int, DecWs *, b64_result *);
 
 EncFn enc_table[3][3] = {
-    {encode_kernel<16, 16, false>, encode_kernel<16, 4, false>, encode_kernel<16, 1, false>},
-    {encode_kernel<4, 16, false>, encode_kernel<4, 4, false>, encode_kernel<4, 1, false>},
-    {encode_kernel<1, 16, false>, encode_kernel<1, 4, false>, encode_kernel<1, 1, false>},
+    {encode_kernel<16, 16>, encode_kernel<16, 4>, encode_kernel<16, 1>},
+    {encode_kernel<4, 16>, encode_kernel<4, 4>, encode_kernel<4, 1>},
+    {encode_kernel<1, 16>, encode_kernel<1, 4>, encode_kernel<1, 1>},
 };
 DecFn dec_table[3][3] = {
-    {decode_kernel<16, 16, false>, decode_kernel<16, 4, false>, decode_kernel<16, 1, false>},
-    {decode_kernel<4, 16, false>, decode_kernel<4, 4, false>, decode_kernel<4, 1, false>},
-    {decode_kernel<1, 16, false>, decode_kernel<1, 4, false>, decode_kernel<1, 1, false>},
+    {decode_kernel<16, 16>, decode_kernel<16, 4>, decode_kernel<16, 1>},
+    {decode_kernel<4, 16>, decode_kernel<4, 4>, decode_kernel<4, 1>},
+    {decode_kernel<1, 16>, decode_kernel<1, 4>, decode_kernel<1, 1>},
 };
+constexpr size_t kEncRingBytes = sizeof(EncRing) * kBWarps;
+constexpr size_t kDecRingBytes = sizeof(DecRing) * kBWarps;
 
 int align_class(const void *p) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
@@ -607,12 +373,12 @@ bool device_setup(int *dev_out, int *sms_out) {
       return false;
     for (auto &row : enc_table)
       for (auto f : row)
-        if (set_smem(f, sizeof(EncSmem<false>)) != cudaSuccess) return false;
+        if (set_smem(f, sizeof(EncSmem)) != cudaSuccess) return false;
     for (auto &row : dec_table)
       for (auto f : row)
-        if (set_smem(f, sizeof(DecSmem<false>)) != cudaSuccess) return false;
-    if (set_smem(encode_kernel<1, 1, true>, sizeof(EncSmem<true>)) != cudaSuccess) return false;
-    if (set_smem(decode_kernel<1, 1, true>, sizeof(DecSmem<true>)) != cudaSuccess) return false;
+        if (set_smem(f, sizeof(DecSmem)) != cudaSuccess) return false;
+    if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return false;
+    if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return false;
     di.attrs_set = true;
   }
   *dev_out = dev;
@@ -649,25 +415,20 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
   const int64_t ntiles = (chars + DecS1::kIn - 1) / DecS1::kIn;
   const int64_t grid = grid_for(ntiles, sms);
   DecFn f = dec_table[align_class(d_in)][align_class(d_out)];
-  f<<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem<false>), stream>>>(
-      d_in, m, d_out, ntiles, final_shard, ws, d_result, nullptr, nullptr, nullptr, nullptr,
-      nullptr, nullptr, nullptr, nullptr);
+  f<<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem), stream>>>(d_in, m, d_out, ntiles,
+                                                                        final_shard, ws, d_result);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
-size_t ws_layout(int64_t k, int64_t total_in, int direction, size_t *off_descs, size_t *off_done,
-                 int64_t *cap) {
-  const int64_t tile = direction ? DecGeo<true>::kIn : EncGeo<true>::kIn;
-  const int64_t c = (total_in > 0 ? total_in / tile : 0) + k + 1;
-  size_t o = 256;  // PlanHeader
-  *off_descs = o;
-  o += static_cast<size_t>(c) * sizeof(TileDesc);
+// Batched workspace: [BatchHeader | unit_off[k+1] (int64) | msg_done[k] (u32)].
+size_t ws_layout(int64_t k, size_t *off_units, size_t *off_done) {
+  size_t o = 256;
+  *off_units = o;
+  o += static_cast<size_t>(k + 1) * sizeof(int64_t);
   o = (o + 255) & ~static_cast<size_t>(255);
   *off_done = o;
   o += static_cast<size_t>(k > 0 ? k : 1) * sizeof(unsigned int);
-  o = (o + 255) & ~static_cast<size_t>(255);
-  *cap = c;
-  return o;
+  return (o + 255) & ~static_cast<size_t>(255);
 }
 
 }  // namespace
@@ -689,8 +450,7 @@ int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t 
   const int64_t ntiles = (n + EncS1::kIn - 1) / EncS1::kIn;
   const int64_t grid = grid_for(ntiles, sms);
   EncFn f = enc_table[align_class(d_in)][align_class(d_out)];
-  f<<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem<false>), stream>>>(d_in, n, d_out, ntiles,
-                                                                          nullptr, nullptr);
+  f<<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem), stream>>>(d_in, n, d_out, ntiles);
   if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
   return 4 * ((n + 2) / 3);
 }
@@ -732,9 +492,9 @@ int b64_decode(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *out_len,
 
 size_t b64_batch_workspace_bytes(int64_t k, int64_t total_in, int direction) {
   if (k < 0 || total_in < 0) return 0;
+  (void)direction;
   size_t a, b;
-  int64_t cap;
-  return ws_layout(k, total_in, direction ? 1 : 0, &a, &b, &cap);
+  return ws_layout(k, &a, &b);
 }
 
 static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
@@ -747,37 +507,31 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
     return B64_ERR_ARG;
   if (k > INT32_MAX) return B64_ERR_ARG;
   if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) return B64_ERR_ARG;
-  size_t off_descs, off_done;
-  int64_t cap;
-  const size_t need = ws_layout(k, total_in, direction, &off_descs, &off_done, &cap);
+  size_t off_units, off_done;
+  const size_t need = ws_layout(k, &off_units, &off_done);
   if (ws_bytes < need) return B64_ERR_WORKSPACE;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   uint8_t *ws = static_cast<uint8_t *>(d_ws);
-  PlanHeader *hdr = reinterpret_cast<PlanHeader *>(ws);
-  TileDesc *descs = reinterpret_cast<TileDesc *>(ws + off_descs);
+  BatchHeader *hdr = reinterpret_cast<BatchHeader *>(ws);
+  int64_t *unit_off = reinterpret_cast<int64_t *>(ws + off_units);
   unsigned int *done = reinterpret_cast<unsigned int *>(ws + off_done);
-  PlanHeader h{0, cap, 0, 0};
-  if (cudaMemcpyAsync(hdr, &h, sizeof(h), cudaMemcpyHostToDevice, stream) != cudaSuccess)
-    return B64_ERR_CUDA;
   if (direction) {
-    plan_kernel<true><<<1, kPlanThreads, 0, stream>>>(d_in, d_in_off, k, d_out_off, hdr, descs,
+    plan_kernel<true><<<1, kPlanThreads, 0, stream>>>(d_in, d_in_off, k, d_out_off, unit_off, hdr,
                                                        d_err_pos, d_out_len, d_status, done);
   } else {
-    plan_kernel<false><<<1, kPlanThreads, 0, stream>>>(d_in, d_in_off, k, d_out_off, hdr, descs,
+    plan_kernel<false><<<1, kPlanThreads, 0, stream>>>(d_in, d_in_off, k, d_out_off, unit_off, hdr,
                                                         nullptr, nullptr, nullptr, done);
   }
   if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
-  const int64_t tile = direction ? DecGeo<true>::kIn : EncGeo<true>::kIn;
-  const int64_t max_tiles = total_in / tile + k;
-  const int64_t grid = grid_for(max_tiles, sms);
+  if (k == 0) return B64_OK;
+  const unsigned grid = static_cast<unsigned>(sms);
   if (direction) {
-    decode_kernel<1, 1, true><<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem<true>), stream>>>(
-        d_in, 0, d_out, 0, 1, nullptr, nullptr, descs, &hdr->ntiles, d_in_off, d_out_off,
-        d_err_pos, d_out_len, d_status, done);
+    batch_kernel<true><<<grid, kBThreads, kDecRingBytes, stream>>>(
+        d_in, d_out, k, d_in_off, d_out_off, unit_off, hdr, d_err_pos, d_out_len, d_status, done);
   } else {
-    encode_kernel<1, 1, true><<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem<true>), stream>>>(
-        d_in, 0, d_out, 0, descs, &hdr->ntiles);
+    batch_kernel<false><<<grid, kBThreads, kEncRingBytes, stream>>>(
+        d_in, d_out, k, d_in_off, d_out_off, unit_off, hdr, nullptr, nullptr, nullptr, done);
   }
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
