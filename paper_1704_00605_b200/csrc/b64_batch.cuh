@@ -19,6 +19,8 @@
 #include <cstdint>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "b64_codec.cuh"
 #include "b64_ptx.cuh"
 
@@ -72,12 +74,13 @@ struct BatchHeader {
 };
 
 // ------------------------------------------------------------- planner ---
-// One CTA of 1024 threads, ITEMS consecutive messages per thread per round.
-// Round = (1) per-thread sums of output sizes and unit counts, (2) block
-// exclusive scan, (3) re-walk the thread's messages writing out_off,
-// unit_off and (decode) the per-message result initialisation.
-constexpr int kPlanThreads = 1024;
-constexpr int kPlanItems = 10;
+// The plan (exclusive scans of per-message output sizes and unit counts) is
+// phase 1 of the same cooperative launch: CTA b scans messages
+// [b*chunk, (b+1)*chunk) in rounds of one message per thread, publishes its
+// totals, grid-syncs, adds the totals of CTAs < b and writes out_off /
+// unit_off (and the decode per-message result initialisation); a second
+// grid sync publishes the plan to every warp.  No planner launch, no
+// descriptor array.
 
 __device__ __forceinline__ void block_exclusive_scan2(int64_t a, int64_t b, int64_t &pa,
                                                       int64_t &pb, int64_t &ta, int64_t &tb,
@@ -99,7 +102,8 @@ __device__ __forceinline__ void block_exclusive_scan2(int64_t a, int64_t b, int6
   }
   __syncthreads();
   if (warp == 0) {
-    const int64_t wa = sh[lane], wb = sh[32 + lane];
+    const int nw = static_cast<int>(blockDim.x >> 5);
+    const int64_t wa = lane < nw ? sh[lane] : 0, wb = lane < nw ? sh[32 + lane] : 0;
     int64_t sa = wa, sb = wb;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -139,58 +143,6 @@ __device__ __forceinline__ void msg_sizes(const uint8_t *in, int64_t a, int64_t 
   } else {
     osz = 4 * ((len + 2) / 3);
     units = (len + EU::kIn - 1) / EU::kIn;
-  }
-}
-
-template <bool DECODE>
-__global__ void __launch_bounds__(kPlanThreads)
-    plan_kernel(const uint8_t *__restrict__ in, const int64_t *__restrict__ in_off, int64_t k,
-                int64_t *__restrict__ out_off, int64_t *__restrict__ unit_off, BatchHeader *hdr,
-                int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
-                int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
-  __shared__ int64_t sh[66];
-  int64_t carry_o = 0, carry_u = 0;
-  for (int64_t base = 0; base < k; base += static_cast<int64_t>(kPlanThreads) * kPlanItems) {
-    const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * kPlanItems;
-    const int nit = static_cast<int>(i0 >= k ? 0 : (k - i0 < kPlanItems ? k - i0 : kPlanItems));
-    int64_t so = 0, su = 0;
-    for (int t = 0; t < nit; ++t) {
-      int64_t o, u;
-      msg_sizes<DECODE>(in, in_off[i0 + t], in_off[i0 + t + 1], o, u);
-      so += o;
-      su += u;
-    }
-    int64_t po, pu, to, tu;
-    block_exclusive_scan2(so, su, po, pu, to, tu, sh);
-    int64_t ro = carry_o + po, ru = carry_u + pu;
-    for (int t = 0; t < nit; ++t) {
-      const int64_t i = i0 + t;
-      const int64_t a = in_off[i], b = in_off[i + 1];
-      int64_t o, u;
-      msg_sizes<DECODE>(in, a, b, o, u);
-      out_off[i] = ro;
-      unit_off[i] = ru;
-      if (DECODE) {
-        msg_done[i] = 0;
-        const int64_t len = b - a;
-        if (u == 0) {  // no complete quad: the result is decided here
-          status[i] = (len & 3) ? B64_ERR_LENGTH : B64_OK;
-          err_pos[i] = (len & 3) ? 0 : -1;
-          out_len[i] = 0;
-        } else {
-          err_pos[i] = LLONG_MAX;
-        }
-      }
-      ro += o;
-      ru += u;
-    }
-    carry_o += to;
-    carry_u += tu;
-  }
-  if (threadIdx.x == 0) {
-    out_off[k] = carry_o;
-    unit_off[k] = carry_u;
-    hdr->nunits = carry_u;
   }
 }
 
@@ -259,16 +211,18 @@ __device__ __forceinline__ void warp_copy_out(uint8_t *gdst, const uint8_t *sbuf
 template <bool DECODE>
 __global__ void __launch_bounds__(kBThreads, 1)
     batch_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t k,
-                 const int64_t *__restrict__ in_off, const int64_t *__restrict__ out_off,
-                 const int64_t *__restrict__ unit_off, const BatchHeader *__restrict__ hdr,
+                 const int64_t *__restrict__ in_off, int64_t *__restrict__ out_off,
+                 int64_t *__restrict__ unit_off, int64_t *__restrict__ blk,
                  int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
                  int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
   using Ring = typename std::conditional<DECODE, DecRing, EncRing>::type;
   constexpr int UIN = DECODE ? DU::kIn : EU::kIn;
   constexpr int UOUT = DECODE ? DU::kOut : EU::kOut;
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ int64_t sh[66];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Ring &R = reinterpret_cast<Ring *>(smem_raw)[warp];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
 
   if (DECODE) {
     if (tid < 256) g_dec_tab[tid] = kInvalid;
@@ -281,9 +235,83 @@ __global__ void __launch_bounds__(kBThreads, 1)
     for (int s = 0; s < kBSlots; ++s) mbar_init(&R.full[s], 1);
     fence_mbar_init();
   }
-  __syncthreads();
 
-  const int64_t U = hdr->nunits;
+  // ---- phase 1: plan (exclusive scans), see header comment
+  const int64_t G = gridDim.x;
+  const int64_t chunk = (k + G - 1) / G;
+  const int64_t i_lo = blockIdx.x * chunk < k ? blockIdx.x * chunk : k;
+  const int64_t i_hi = i_lo + chunk < k ? i_lo + chunk : k;
+  int64_t tot_o = 0, tot_u = 0;
+  for (int64_t r0 = i_lo; r0 < i_hi; r0 += kBThreads) {
+    const int64_t i = r0 + tid;
+    int64_t o = 0, u = 0;
+    if (i < i_hi) msg_sizes<DECODE>(in, in_off[i], in_off[i + 1], o, u);
+    int64_t po, pu, to, tu;
+    block_exclusive_scan2(o, u, po, pu, to, tu, sh);
+    tot_o += to;
+    tot_u += tu;
+  }
+  if (tid == 0) {
+    blk[2 * blockIdx.x] = tot_o;
+    blk[2 * blockIdx.x + 1] = tot_u;
+  }
+  grid.sync();
+  // offsets of this CTA = sum of the totals of CTAs < blockIdx.x; U = all
+  int64_t bo = 0, bu = 0, all_u = 0;
+  for (int64_t b = tid; b < G; b += kBThreads) {
+    const int64_t to = blk[2 * b], tu = blk[2 * b + 1];
+    if (b < blockIdx.x) {
+      bo += to;
+      bu += tu;
+    }
+    all_u += tu;
+  }
+  {
+    int64_t p1, p2, t1, t2;
+    block_exclusive_scan2(bo, bu, p1, p2, t1, t2, sh);
+    bo = t1;
+    bu = t2;
+    int64_t q1, q2, t3, t4;
+    block_exclusive_scan2(all_u, 0, q1, q2, t3, t4, sh);
+    all_u = t3;
+  }
+  for (int64_t r0 = i_lo; r0 < i_hi; r0 += kBThreads) {
+    const int64_t i = r0 + tid;
+    int64_t o = 0, u = 0, a = 0, b = 0;
+    if (i < i_hi) {
+      a = in_off[i];
+      b = in_off[i + 1];
+      msg_sizes<DECODE>(in, a, b, o, u);
+    }
+    int64_t po, pu, to, tu;
+    block_exclusive_scan2(o, u, po, pu, to, tu, sh);
+    if (i < i_hi) {
+      out_off[i] = bo + po;
+      unit_off[i] = bu + pu;
+      if (DECODE) {
+        msg_done[i] = 0;
+        const int64_t len = b - a;
+        if (u == 0) {  // no complete quad: the result is decided here
+          status[i] = (len & 3) ? B64_ERR_LENGTH : B64_OK;
+          err_pos[i] = (len & 3) ? 0 : -1;
+          out_len[i] = 0;
+        } else {
+          err_pos[i] = LLONG_MAX;
+        }
+      }
+    }
+    bo += to;
+    bu += tu;
+  }
+  if (blockIdx.x == G - 1 && tid == 0) {
+    out_off[k] = bo;
+    unit_off[k] = bu;
+  }
+  __threadfence();
+  grid.sync();
+
+  // ---- phase 2: warps take equal contiguous unit ranges
+  const int64_t U = all_u;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kBWarps + warp;
   const int64_t GW = static_cast<int64_t>(gridDim.x) * kBWarps;
   const int64_t u_begin = static_cast<int64_t>((static_cast<__int128>(U) * gw) / GW);
@@ -382,18 +410,16 @@ __global__ void __launch_bounds__(kBThreads, 1)
     warp_copy_out(gdst, R.out + omis, olen, lane);
     if constexpr (DECODE) {
       if (lane == 0) {
-        if (werr != 0xFFFFFFFFu) {
+        if (werr != 0xFFFFFFFFu && d.nunits > 1) {
           unsigned long long *tgt = reinterpret_cast<unsigned long long *>(err_pos + d.msg);
           const unsigned long long pos = static_cast<unsigned long long>(d.rel) + werr;
           if (pos < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, pos);
+          __threadfence();  // order the error before this unit's completion count
         }
         // Per-message completion: the warp finishing the message's last
         // unit writes its result (status is a pure function of err_pos).
         bool mine = d.nunits == 1;
-        if (!mine) {
-          __threadfence();
-          mine = atomicAdd(msg_done + d.msg, 1u) == static_cast<unsigned>(d.nunits - 1);
-        }
+        if (!mine) mine = atomicAdd(msg_done + d.msg, 1u) == static_cast<unsigned>(d.nunits - 1);
         if (mine) {
           __threadfence();
           const int64_t i = d.msg;

@@ -189,13 +189,15 @@ __device__ __forceinline__ void st_global_v4(uint8_t *p, const uint4 &v) {
 // (s_{i+1}*4 mod 64) + s_{i+2}/64 and s_{i+2} mod 64, i.e. bits 23..18,
 // 17..12, 11..6, 5..0 of x; each is mapped through the 64-entry smem table B
 // and the four characters are packed little-endian (first char = byte 0).
+// g_enc_tab is 64-byte aligned, so each lookup address is the 6-bit field
+// OR-ed into the table base (SHF + LOP3, or one LOP3 / LEA.HI).
 template <bool TOPZERO>
-__device__ __forceinline__ uint32_t enc_group(uint32_t x) {
-  const uint32_t i0 = TOPZERO ? (x >> 18) : ((x >> 18) & 63u);
-  const uint32_t i1 = (x >> 12) & 63u;
-  const uint32_t i2 = (x >> 6) & 63u;
-  const uint32_t i3 = x & 63u;
-  const uint32_t c0 = g_enc_tab[i0], c1 = g_enc_tab[i1], c2 = g_enc_tab[i2], c3 = g_enc_tab[i3];
+__device__ __forceinline__ uint32_t enc_group(uint32_t x, uint32_t tb) {
+  const uint32_t a0 = TOPZERO ? ((x >> 18) | tb) : (((x >> 18) & 63u) | tb);
+  const uint32_t a1 = ((x >> 12) & 63u) | tb;
+  const uint32_t a2 = ((x >> 6) & 63u) | tb;
+  const uint32_t a3 = (x & 63u) | tb;
+  const uint32_t c0 = lds_u8(a0), c1 = lds_u8(a1), c2 = lds_u8(a2), c3 = lds_u8(a3);
   return __byte_perm(__byte_perm(c0, c1, 0x3340), __byte_perm(c2, c3, 0x3340), 0x5410);
 }
 
@@ -203,10 +205,11 @@ __device__ __forceinline__ uint32_t enc_group(uint32_t x) {
 // __byte_perm reorders each 3-byte group big-endian (the GPU counterpart of
 // the paper's vpshufb step in enc_reshuffle).
 __device__ __forceinline__ void encode12(const uint32_t (&w)[3], uint32_t (&c)[4]) {
-  c[0] = enc_group<true>(__byte_perm(w[0], 0u, 0x4012));    // b0 b1 b2
-  c[1] = enc_group<false>(__byte_perm(w[0], w[1], 0x3345));  // b3 b4 b5
-  c[2] = enc_group<false>(__byte_perm(w[1], w[2], 0x2234));  // b6 b7 b8
-  c[3] = enc_group<true>(__byte_perm(w[2], 0u, 0x4123));    // b9 b10 b11
+  const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(g_enc_tab));
+  c[0] = enc_group<true>(__byte_perm(w[0], 0u, 0x4012), tb);    // b0 b1 b2
+  c[1] = enc_group<false>(__byte_perm(w[0], w[1], 0x3345), tb);  // b3 b4 b5
+  c[2] = enc_group<false>(__byte_perm(w[1], w[2], 0x2234), tb);  // b6 b7 b8
+  c[3] = enc_group<true>(__byte_perm(w[2], 0u, 0x4123), tb);    // b9 b10 b11
 }
 
 // Replace byte i (0..15) of the 4-word vector with value v.

@@ -420,9 +420,11 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
-// Batched workspace: [BatchHeader | unit_off[k+1] (int64) | msg_done[k] (u32)].
+// Batched workspace: [per-CTA totals (2 x 1024 int64) | unit_off[k+1] (int64)
+// | msg_done[k] (u32)].
+constexpr int kMaxBatchCtas = 1024;
 size_t ws_layout(int64_t k, size_t *off_units, size_t *off_done) {
-  size_t o = 256;
+  size_t o = 2 * kMaxBatchCtas * sizeof(int64_t);
   *off_units = o;
   o += static_cast<size_t>(k + 1) * sizeof(int64_t);
   o = (o + 255) & ~static_cast<size_t>(255);
@@ -513,26 +515,37 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   uint8_t *ws = static_cast<uint8_t *>(d_ws);
-  BatchHeader *hdr = reinterpret_cast<BatchHeader *>(ws);
+  int64_t *blk = reinterpret_cast<int64_t *>(ws);
   int64_t *unit_off = reinterpret_cast<int64_t *>(ws + off_units);
   unsigned int *done = reinterpret_cast<unsigned int *>(ws + off_done);
-  if (direction) {
-    plan_kernel<true><<<1, kPlanThreads, 0, stream>>>(d_in, d_in_off, k, d_out_off, unit_off, hdr,
-                                                       d_err_pos, d_out_len, d_status, done);
-  } else {
-    plan_kernel<false><<<1, kPlanThreads, 0, stream>>>(d_in, d_in_off, k, d_out_off, unit_off, hdr,
-                                                        nullptr, nullptr, nullptr, done);
+  if (k == 0) {
+    // nothing to plan: d_out_off[0] = 0
+    const int64_t zero = 0;
+    return cudaMemcpyAsync(d_out_off, &zero, sizeof(zero), cudaMemcpyHostToDevice, stream) == cudaSuccess
+               ? B64_OK
+               : B64_ERR_CUDA;
   }
-  if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
-  if (k == 0) return B64_OK;
-  const unsigned grid = static_cast<unsigned>(sms);
+  // One cooperative launch: plan + grid sync + codec (all CTAs co-resident).
+  const unsigned grid = static_cast<unsigned>(sms < kMaxBatchCtas ? sms : kMaxBatchCtas);
+  const uint8_t *a_in = d_in;
+  uint8_t *a_out = d_out;
+  int64_t a_k = k;
+  const int64_t *a_in_off = d_in_off;
+  int64_t *a_out_off = d_out_off, *a_unit = unit_off, *a_blk = blk;
+  int64_t *a_err = d_err_pos, *a_len = d_out_len;
+  int32_t *a_st = d_status;
+  unsigned int *a_done = done;
+  void *args[] = {&a_in, &a_out, &a_k, &a_in_off, &a_out_off, &a_unit, &a_blk,
+                  &a_err, &a_len, &a_st, &a_done};
+  cudaError_t e;
   if (direction) {
-    batch_kernel<true><<<grid, kBThreads, kDecRingBytes, stream>>>(
-        d_in, d_out, k, d_in_off, d_out_off, unit_off, hdr, d_err_pos, d_out_len, d_status, done);
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(batch_kernel<true>), dim3(grid),
+                                    dim3(kBThreads), args, kDecRingBytes, stream);
   } else {
-    batch_kernel<false><<<grid, kBThreads, kEncRingBytes, stream>>>(
-        d_in, d_out, k, d_in_off, d_out_off, unit_off, hdr, nullptr, nullptr, nullptr, done);
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(batch_kernel<false>), dim3(grid),
+                                    dim3(kBThreads), args, kEncRingBytes, stream);
   }
+  if (e != cudaSuccess) return B64_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
