@@ -30,6 +30,7 @@ using namespace ptx;
 
 constexpr int kBWarps = B64_BATCH_WARPS;
 constexpr int kBSlots = B64_BATCH_SLOTS;
+static_assert((kBSlots & (kBSlots - 1)) == 0, "batch ring depth must be a power of two");
 constexpr int kBThreads = kBWarps * 32;
 constexpr int kFlagLast = 2;  // unit is the last unit of its message
 
@@ -50,7 +51,9 @@ struct UnitDesc {
   int64_t src;     // input offset of the unit (relative to d_in)
   int64_t dst;     // output offset (relative to d_out)
   int64_t rel;     // input offset of the unit within its message
-  int32_t len;     // input bytes of the unit (decode: multiple of 4, may be 0 < len)
+  int64_t mlen;    // message length (input bytes)
+  int64_t mcap;    // message output reservation (out_off[i+1] - out_off[i])
+  int32_t len;     // input bytes of the unit (decode: multiple of 4, > 0)
   int32_t msg;     // message index
   int32_t flags;   // kFlagLast | kFlagFinal
   int32_t nunits;  // units of the message
@@ -325,7 +328,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
   window_load(win, msg, k, in_off, out_off, unit_off, lane);
   auto field = [&](int64_t v, int64_t j) { return __shfl_sync(0xffffffffu, v, static_cast<int>(j - win.base)); };
   int64_t m_in = field(win.io, msg), m_end = field(win.io, msg + 1);
-  int64_t m_out = field(win.oo, msg), m_u0 = field(win.uo, msg), m_u1 = field(win.uo, msg + 1);
+  int64_t m_out = field(win.oo, msg), m_oend = field(win.oo, msg + 1);
+  int64_t m_u0 = field(win.uo, msg), m_u1 = field(win.uo, msg + 1);
 
   auto issue = [&](int64_t u) {
     while (u >= m_u1) {  // advance to the message holding unit u (skips empty messages)
@@ -334,6 +338,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       m_in = field(win.io, msg);
       m_end = field(win.io, msg + 1);
       m_out = field(win.oo, msg);
+      m_oend = field(win.oo, msg + 1);
       m_u0 = field(win.uo, msg);
       m_u1 = field(win.uo, msg + 1);
     }
@@ -348,10 +353,12 @@ __global__ void __launch_bounds__(kBThreads, 1)
     d.len = static_cast<int32_t>(left < UIN ? left : UIN);
     d.msg = static_cast<int32_t>(msg);
     d.nunits = static_cast<int32_t>(m_u1 - m_u0);
+    d.mlen = mlen;
+    d.mcap = m_oend - m_out;
     const bool last = u == m_u1 - 1;
     d.flags = (last ? kFlagLast : 0) | ((DECODE && last && (mlen & 3) == 0) ? kFlagFinal : 0);
     if (lane == 0) {
-      const int s = static_cast<int>((u - u_begin) % kBSlots);
+      const int s = static_cast<int>(u - u_begin) & (kBSlots - 1);
       R.desc[s] = d;
       const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
       const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
@@ -365,12 +372,54 @@ __global__ void __launch_bounds__(kBThreads, 1)
   int64_t iu = u_begin;
   for (; iu < u_end && iu < u_begin + kBSlots; ++iu) issue(iu);
 
-  for (int64_t cu = u_begin; cu < u_end; ++cu) {
-    const int64_t it = cu - u_begin;
-    const int s = static_cast<int>(it % kBSlots);
+  // Decode: per-message error / completion accounting over the span of
+  // consecutive units this warp processes (one flush per message span).
+  int32_t sp_msg = -1, sp_cnt = 0, sp_n = 0;
+  unsigned long long sp_err = static_cast<unsigned long long>(LLONG_MAX);
+  int64_t sp_mlen = 0, sp_mcap = 0;
+  auto flush = [&]() {
+    if (!DECODE || sp_msg < 0 || lane != 0) return;
+    const int64_t i = sp_msg;
+    bool mine = sp_cnt == sp_n;  // this warp decoded the whole message
+    unsigned long long e = sp_err;
+    if (!mine) {
+      if (sp_err != static_cast<unsigned long long>(LLONG_MAX)) {
+        unsigned long long *tgt = reinterpret_cast<unsigned long long *>(err_pos + i);
+        if (sp_err < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, sp_err);
+      }
+      __threadfence();  // order the error before the completion count
+      mine = atomicAdd(msg_done + i, static_cast<unsigned>(sp_cnt)) + sp_cnt == static_cast<unsigned>(sp_n);
+      if (mine) {
+        __threadfence();
+        e = atomicOr(reinterpret_cast<unsigned long long *>(err_pos + i), 0ull);
+      }
+    }
+    if (mine) {
+      const int64_t q = sp_mlen / 4, r = sp_mlen % 4;
+      int64_t err = e == static_cast<unsigned long long>(LLONG_MAX) ? -1 : static_cast<int64_t>(e);
+      if (err < 0 && r != 0) err = 4 * q;
+      if (err < 0) {
+        status[i] = B64_OK;
+        out_len[i] = sp_mcap;
+      } else if (r != 0 && err == 4 * q) {
+        status[i] = B64_ERR_LENGTH;
+        out_len[i] = 3 * q;
+      } else {
+        status[i] = B64_ERR_INVALID_CHAR;
+        out_len[i] = 3 * (err / 4);
+      }
+      err_pos[i] = err;
+    }
+  };
+
+  const int32_t nu = static_cast<int32_t>(u_end - u_begin);
+  for (int32_t it = 0; it < nu; ++it) {
+    const int s = it & (kBSlots - 1);
     mbar_wait_spin(&R.full[s], static_cast<uint32_t>((it / kBSlots) & 1));
     const UnitDesc d = R.desc[s];
-    const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + d.src) & 15);
+    const uintptr_t gsrc = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
+    const int imis = static_cast<int>(gsrc & 15);
+    const bool in4 = (gsrc & 3) == 0;
     const uint8_t *sin = R.in[s] + imis;
     uint8_t *gdst = out + d.dst;
     const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
@@ -378,10 +427,14 @@ __global__ void __launch_bounds__(kBThreads, 1)
     int olen;
     uint32_t werr = 0xFFFFFFFFu;
     if constexpr (!DECODE) {
-      if (d.len == UIN)
-        encode_tile<1, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
-      else
+      if (d.len == UIN) {
+        if (in4)
+          encode_tile<4, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+        else
+          encode_tile<1, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+      } else {
         encode_tile<1, 1, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+      }
       olen = 4 * ((d.len + 2) / 3);
     } else {
       const bool fin = (d.flags & kFlagFinal) != 0;
@@ -392,11 +445,15 @@ __global__ void __launch_bounds__(kBThreads, 1)
         ch2 = sin[d.len - 2];
         pads = ch1 == '=' ? (ch2 == '=' ? 2 : 1) : 0;
       }
-      werr = (d.len == UIN && !fin)
-                 ? decode_tile<1, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
-                                                                     false, 0, 0)
-                 : decode_tile<1, 1, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
-                                                                      fin, ch2, ch1);
+      if (d.len == UIN && !fin) {
+        werr = in4 ? decode_tile<4, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
+                                                                      false, 0, 0)
+                   : decode_tile<1, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
+                                                                      false, 0, 0);
+      } else {
+        werr = decode_tile<1, 1, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
+                                                                 fin, ch2, ch1);
+      }
       olen = 3 * (d.len / 4) - pads;
     }
     __syncwarp();
@@ -409,45 +466,28 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
     warp_copy_out(gdst, R.out + omis, olen, lane);
     if constexpr (DECODE) {
-      if (lane == 0) {
-        if (werr != 0xFFFFFFFFu && d.nunits > 1) {
-          unsigned long long *tgt = reinterpret_cast<unsigned long long *>(err_pos + d.msg);
-          const unsigned long long pos = static_cast<unsigned long long>(d.rel) + werr;
-          if (pos < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, pos);
-          __threadfence();  // order the error before this unit's completion count
-        }
-        // Per-message completion: the warp finishing the message's last
-        // unit writes its result (status is a pure function of err_pos).
-        bool mine = d.nunits == 1;
-        if (!mine) mine = atomicAdd(msg_done + d.msg, 1u) == static_cast<unsigned>(d.nunits - 1);
-        if (mine) {
-          __threadfence();
-          const int64_t i = d.msg;
-          const int64_t len = in_off[i + 1] - in_off[i];
-          const int64_t q = len / 4, r = len % 4;
-          const int64_t cap = out_off[i + 1] - out_off[i];
-          const unsigned long long e =
-              d.nunits == 1 ? (werr != 0xFFFFFFFFu ? static_cast<unsigned long long>(d.rel) + werr
-                                                   : static_cast<unsigned long long>(LLONG_MAX))
-                            : atomicOr(reinterpret_cast<unsigned long long *>(err_pos + i), 0ull);
-          int64_t err = e == static_cast<unsigned long long>(LLONG_MAX) ? -1 : static_cast<int64_t>(e);
-          if (err < 0 && r != 0) err = 4 * q;
-          if (err < 0) {
-            status[i] = B64_OK;
-            out_len[i] = cap;
-          } else if (r != 0 && err == 4 * q) {
-            status[i] = B64_ERR_LENGTH;
-            out_len[i] = 3 * q;
-          } else {
-            status[i] = B64_ERR_INVALID_CHAR;
-            out_len[i] = 3 * (err / 4);
-          }
-          err_pos[i] = err;
-        }
+      if (d.msg != sp_msg) {
+        flush();
+        sp_msg = d.msg;
+        sp_cnt = 0;
+        sp_n = d.nunits;
+        sp_err = static_cast<unsigned long long>(LLONG_MAX);
+        sp_mlen = d.mlen;
+        sp_mcap = d.mcap;
+      }
+      ++sp_cnt;
+      if (werr != 0xFFFFFFFFu) {
+        const unsigned long long pos = static_cast<unsigned long long>(d.rel) + werr;
+        sp_err = pos < sp_err ? pos : sp_err;
+      }
+      if (d.flags & kFlagLast) {
+        flush();
+        sp_msg = -1;
       }
     }
     __syncwarp();
   }
+  flush();
 }
 
 }  // namespace b64
