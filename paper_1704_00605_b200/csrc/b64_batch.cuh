@@ -62,7 +62,7 @@ struct UnitDesc {
 template <int IN, int OUT>
 struct alignas(16) WarpRing {
   static constexpr int kInStride = round_up_c(IN + 32, 16);
-  static constexpr int kOutStride = round_up_c(OUT + 32, 16);
+  static constexpr int kOutStride = round_up_c(OUT + 48, 16);  // 16 head room + 32 read slack
   uint8_t in[kBSlots][kInStride];
   uint8_t out[kOutStride];
   UnitDesc desc[kBSlots];
@@ -188,25 +188,44 @@ __device__ __forceinline__ int64_t find_message(const int64_t *unit_off, int64_t
   return lo;
 }
 
-// Unit-level copy-out: `len` bytes staged at sbuf (same address mod 16 as
-// gdst) -> gdst: interior 16-byte granules by the lanes, edges byte-wise.
-__device__ __forceinline__ void warp_copy_out(uint8_t *gdst, const uint8_t *sbuf, int len,
+// 16 stream bytes starting at byte offset `so` (any alignment) of a
+// 16-byte aligned smem stream: two conflict-free LDS.128 + a uniform
+// word select + funnel shift.
+__device__ __forceinline__ uint4 lds16_unaligned(const uint8_t *stream, int so) {
+  const uint8_t *c = stream + (so & ~15);
+  const uint4 a = *reinterpret_cast<const uint4 *>(c);
+  const uint4 b = *reinterpret_cast<const uint4 *>(c + 16);
+  const uint32_t bs = 8u * static_cast<uint32_t>(so & 3);
+  uint32_t x0, x1, x2, x3, x4;
+  switch ((so >> 2) & 3) {  // warp-uniform
+    case 0: x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w; x4 = b.x; break;
+    case 1: x0 = a.y; x1 = a.z; x2 = a.w; x3 = b.x; x4 = b.y; break;
+    case 2: x0 = a.z; x1 = a.w; x2 = b.x; x3 = b.y; x4 = b.z; break;
+    default: x0 = a.w; x1 = b.x; x2 = b.y; x3 = b.z; x4 = b.w; break;
+  }
+  return make_uint4(__funnelshift_r(x0, x1, bs), __funnelshift_r(x1, x2, bs),
+                    __funnelshift_r(x2, x3, bs), __funnelshift_r(x3, x4, bs));
+}
+
+// Unit-level copy-out: `len` stream bytes staged at the 16-byte aligned smem
+// `stream` -> gdst (any alignment).  Each lane writes whole 16-byte aligned
+// granules of the destination (realigned from smem, one STG.128); the at
+// most two partial granules at the ends are written byte-wise.
+__device__ __forceinline__ void warp_copy_out(uint8_t *gdst, const uint8_t *stream, int len,
                                               int lane) {
-  const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
-  const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
-  const uintptr_t a1 = (g + static_cast<uintptr_t>(len)) & ~static_cast<uintptr_t>(15);
-  if (a1 > a0) {
-    const int head = static_cast<int>(a0 - g);
-    const int ng = static_cast<int>((a1 - a0) >> 4);
-    for (int q = lane; q < ng; q += 32) {
-      const uint4 v = *reinterpret_cast<const uint4 *>(sbuf + head + 16 * q);
-      *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a0) + 16 * q) = v;
+  const int mis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
+  uint8_t *A0 = gdst - mis;
+  const int ngran = (mis + len + 15) >> 4;
+  for (int i = lane; i < ngran; i += 32) {
+    const int so = 16 * i - mis;  // stream offset of granule i
+    if (so >= 0 && so + 16 <= len) {
+      *reinterpret_cast<uint4 *>(A0 + 16 * i) = lds16_unaligned(stream, so);
+    } else {
+      for (int b = 0; b < 16; ++b) {
+        const int idx = so + b;
+        if (idx >= 0 && idx < len) gdst[idx] = stream[idx];
+      }
     }
-    const int tail0 = static_cast<int>(a1 - g);
-    if (lane < head) gdst[lane] = sbuf[lane];
-    if (lane >= 16 && lane - 16 < len - tail0) gdst[tail0 + lane - 16] = sbuf[tail0 + lane - 16];
-  } else {
-    if (lane < len) gdst[lane] = sbuf[lane];
   }
 }
 
@@ -422,18 +441,17 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const bool in4 = (gsrc & 3) == 0;
     const uint8_t *sin = R.in[s] + imis;
     uint8_t *gdst = out + d.dst;
-    const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
-    uint8_t *sout = R.out + omis;
+    uint8_t *sout = R.out + 16;  // aligned stream (16 bytes of head room for the realigning reads)
     int olen;
     uint32_t werr = 0xFFFFFFFFu;
     if constexpr (!DECODE) {
       if (d.len == UIN) {
         if (in4)
-          encode_tile<4, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+          encode_tile<4, 16, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
         else
-          encode_tile<1, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+          encode_tile<1, 16, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
       } else {
-        encode_tile<1, 1, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+        encode_tile<1, 16, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
       }
       olen = 4 * ((d.len + 2) / 3);
     } else {
@@ -446,12 +464,12 @@ __global__ void __launch_bounds__(kBThreads, 1)
         pads = ch1 == '=' ? (ch2 == '=' ? 2 : 1) : 0;
       }
       if (d.len == UIN && !fin) {
-        werr = in4 ? decode_tile<4, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
+        werr = in4 ? decode_tile<4, 4, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
                                                                       false, 0, 0)
-                   : decode_tile<1, 1, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
+                   : decode_tile<1, 4, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
                                                                       false, 0, 0);
       } else {
-        werr = decode_tile<1, 1, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
+        werr = decode_tile<1, 4, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane,
                                                                  fin, ch2, ch1);
       }
       olen = 3 * (d.len / 4) - pads;
@@ -464,7 +482,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       issue(iu);
       ++iu;
     }
-    warp_copy_out(gdst, R.out + omis, olen, lane);
+    warp_copy_out(gdst, sout, olen, lane);
     if constexpr (DECODE) {
       if (d.msg != sp_msg) {
         flush();
