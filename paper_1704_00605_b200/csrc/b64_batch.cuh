@@ -229,6 +229,29 @@ __device__ __forceinline__ void warp_copy_out(uint8_t *gdst, const uint8_t *stre
   }
 }
 
+// Congruent copy-out: `len` bytes staged at sbuf, which has the same address
+// mod 16 as gdst: interior granules by aligned LDS.128 / STG.128, the
+// unaligned edges byte-wise.
+__device__ __forceinline__ void warp_copy_out_congruent(uint8_t *gdst, const uint8_t *sbuf, int len,
+                                                        int lane) {
+  const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
+  const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
+  const uintptr_t a1 = (g + static_cast<uintptr_t>(len)) & ~static_cast<uintptr_t>(15);
+  if (a1 > a0) {
+    const int head = static_cast<int>(a0 - g);
+    const int ng = static_cast<int>((a1 - a0) >> 4);
+    for (int q = lane; q < ng; q += 32) {
+      const uint4 v = *reinterpret_cast<const uint4 *>(sbuf + head + 16 * q);
+      *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a0) + 16 * q) = v;
+    }
+    const int tail0 = static_cast<int>(a1 - g);
+    if (lane < head) gdst[lane] = sbuf[lane];
+    if (lane >= 16 && lane - 16 < len - tail0) gdst[tail0 + lane - 16] = sbuf[tail0 + lane - 16];
+  } else {
+    if (lane < len) gdst[lane] = sbuf[lane];
+  }
+}
+
 // --------------------------------------------------------- the kernel ---
 template <bool DECODE>
 __global__ void __launch_bounds__(kBThreads, 1)
@@ -441,17 +464,24 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const bool in4 = (gsrc & 3) == 0;
     const uint8_t *sin = R.in[s] + imis;
     uint8_t *gdst = out + d.dst;
-    uint8_t *sout = R.out + 16;  // aligned stream (16 bytes of head room for the realigning reads)
+    // Encode outputs start on 4-byte boundaries (out_off are sums of 4*ceil(len/3)):
+    // stage congruent to the destination (aligned word stores, aligned copy).
+    // Decode outputs start anywhere: stage aligned and realign on copy-out.
+    const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
+    const bool congruent = !DECODE && (omis & 3) == 0;
+    uint8_t *sout = congruent ? R.out + 16 + omis : R.out + 16;
     int olen;
     uint32_t werr = 0xFFFFFFFFu;
     if constexpr (!DECODE) {
-      if (d.len == UIN) {
-        if (in4)
-          encode_tile<4, 16, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
-        else
-          encode_tile<1, 16, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
-      } else {
+      if (!congruent) {  // destination not 4-byte aligned: aligned stream + realigning copy
         encode_tile<1, 16, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+      } else if (d.len == UIN) {
+        if (in4)
+          encode_tile<4, 4, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+        else
+          encode_tile<1, 4, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+      } else {
+        encode_tile<1, 4, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
       }
       olen = 4 * ((d.len + 2) / 3);
     } else {
@@ -482,7 +512,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
       issue(iu);
       ++iu;
     }
-    warp_copy_out(gdst, sout, olen, lane);
+    if (congruent)
+      warp_copy_out_congruent(gdst, sout, olen, lane);
+    else
+      warp_copy_out(gdst, sout, olen, lane);
     if constexpr (DECODE) {
       if (d.msg != sp_msg) {
         flush();
