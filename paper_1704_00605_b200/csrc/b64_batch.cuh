@@ -214,19 +214,20 @@ __device__ __forceinline__ uint4 lds16_unaligned(const uint8_t *stream, int so) 
 __device__ __forceinline__ void warp_copy_out(uint8_t *gdst, const uint8_t *stream, int len,
                                               int lane) {
   const int mis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
-  uint8_t *A0 = gdst - mis;
-  const int ngran = (mis + len + 15) >> 4;
-  for (int i = lane; i < ngran; i += 32) {
-    const int so = 16 * i - mis;  // stream offset of granule i
-    if (so >= 0 && so + 16 <= len) {
-      *reinterpret_cast<uint4 *>(A0 + 16 * i) = lds16_unaligned(stream, so);
-    } else {
-      for (int b = 0; b < 16; ++b) {
-        const int idx = so + b;
-        if (idx >= 0 && idx < len) gdst[idx] = stream[idx];
-      }
-    }
+  const int head = mis ? 16 - mis : 0;        // bytes before the first full granule
+  const int body = (len - head) & ~15;        // full granules
+  if (len <= head + 16) {                      // tiny output: bytes only
+    if (lane < len) gdst[lane] = stream[lane];
+    return;
   }
+  const int ng = body >> 4;
+  uint8_t *B0 = gdst + head;                   // 16-byte aligned
+  for (int i = lane; i < ng; i += 32)
+    *reinterpret_cast<uint4 *>(B0 + 16 * i) = lds16_unaligned(stream, head + 16 * i);
+  // edges: head bytes by lanes 0..15, tail bytes by lanes 16..31
+  const int tail0 = head + body;
+  if (lane < head) gdst[lane] = stream[lane];
+  if (lane >= 16 && tail0 + lane - 16 < len) gdst[tail0 + lane - 16] = stream[tail0 + lane - 16];
 }
 
 // Congruent copy-out: `len` bytes staged at sbuf, which has the same address
@@ -334,7 +335,6 @@ __global__ void __launch_bounds__(kBThreads, 1)
       out_off[i] = bo + po;
       unit_off[i] = bu + pu;
       if (DECODE) {
-        msg_done[i] = 0;
         const int64_t len = b - a;
         if (u == 0) {  // no complete quad: the result is decided here
           status[i] = (len & 3) ? B64_ERR_LENGTH : B64_OK;
@@ -355,14 +355,16 @@ __global__ void __launch_bounds__(kBThreads, 1)
   __threadfence();
   grid.sync();
 
+#ifdef B64_BATCH_PLAN_ONLY  // measurement only (tools/sweep.py): stop after the plan
+  return;
+#endif
   // ---- phase 2: warps take equal contiguous unit ranges
   const int64_t U = all_u;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kBWarps + warp;
   const int64_t GW = static_cast<int64_t>(gridDim.x) * kBWarps;
   const int64_t u_begin = static_cast<int64_t>((static_cast<__int128>(U) * gw) / GW);
   const int64_t u_end = static_cast<int64_t>((static_cast<__int128>(U) * (gw + 1)) / GW);
-  if (u_begin >= u_end) return;
-
+  if (u_begin < u_end) {
   const uint64_t pol = policy_evict_first();
   // ---- issue-side walker state
   MsgWindow win;
@@ -413,46 +415,6 @@ __global__ void __launch_bounds__(kBThreads, 1)
 
   int64_t iu = u_begin;
   for (; iu < u_end && iu < u_begin + kBSlots; ++iu) issue(iu);
-
-  // Decode: per-message error / completion accounting over the span of
-  // consecutive units this warp processes (one flush per message span).
-  int32_t sp_msg = -1, sp_cnt = 0, sp_n = 0;
-  unsigned long long sp_err = static_cast<unsigned long long>(LLONG_MAX);
-  int64_t sp_mlen = 0, sp_mcap = 0;
-  auto flush = [&]() {
-    if (!DECODE || sp_msg < 0 || lane != 0) return;
-    const int64_t i = sp_msg;
-    bool mine = sp_cnt == sp_n;  // this warp decoded the whole message
-    unsigned long long e = sp_err;
-    if (!mine) {
-      if (sp_err != static_cast<unsigned long long>(LLONG_MAX)) {
-        unsigned long long *tgt = reinterpret_cast<unsigned long long *>(err_pos + i);
-        if (sp_err < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, sp_err);
-      }
-      __threadfence();  // order the error before the completion count
-      mine = atomicAdd(msg_done + i, static_cast<unsigned>(sp_cnt)) + sp_cnt == static_cast<unsigned>(sp_n);
-      if (mine) {
-        __threadfence();
-        e = atomicOr(reinterpret_cast<unsigned long long *>(err_pos + i), 0ull);
-      }
-    }
-    if (mine) {
-      const int64_t q = sp_mlen / 4, r = sp_mlen % 4;
-      int64_t err = e == static_cast<unsigned long long>(LLONG_MAX) ? -1 : static_cast<int64_t>(e);
-      if (err < 0 && r != 0) err = 4 * q;
-      if (err < 0) {
-        status[i] = B64_OK;
-        out_len[i] = sp_mcap;
-      } else if (r != 0 && err == 4 * q) {
-        status[i] = B64_ERR_LENGTH;
-        out_len[i] = 3 * q;
-      } else {
-        status[i] = B64_ERR_INVALID_CHAR;
-        out_len[i] = 3 * (err / 4);
-      }
-      err_pos[i] = err;
-    }
-  };
 
   const int32_t nu = static_cast<int32_t>(u_end - u_begin);
   for (int32_t it = 0; it < nu; ++it) {
@@ -517,28 +479,45 @@ __global__ void __launch_bounds__(kBThreads, 1)
     else
       warp_copy_out(gdst, sout, olen, lane);
     if constexpr (DECODE) {
-      if (d.msg != sp_msg) {
-        flush();
-        sp_msg = d.msg;
-        sp_cnt = 0;
-        sp_n = d.nunits;
-        sp_err = static_cast<unsigned long long>(LLONG_MAX);
-        sp_mlen = d.mlen;
-        sp_mcap = d.mcap;
-      }
-      ++sp_cnt;
-      if (werr != 0xFFFFFFFFu) {
+      // First-error reduction: the warp's minimum offset of the
+      // unit, one 64-bit atomicMin on the message's slot (error path only).
+      if (lane == 0 && werr != 0xFFFFFFFFu) {
+        unsigned long long *tgt = reinterpret_cast<unsigned long long *>(err_pos + d.msg);
         const unsigned long long pos = static_cast<unsigned long long>(d.rel) + werr;
-        sp_err = pos < sp_err ? pos : sp_err;
-      }
-      if (d.flags & kFlagLast) {
-        flush();
-        sp_msg = -1;
+        if (pos < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, pos);
       }
     }
     __syncwarp();
   }
-  flush();
+  }  // u_begin < u_end
+
+  if constexpr (DECODE) {
+    // ---- phase 3: per-message results.  After the grid sync every error
+    // atomic has landed; status is a pure function of err_pos (R-length).
+    __threadfence();
+    grid.sync();
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kBThreads + tid; i < k;
+         i += static_cast<int64_t>(gridDim.x) * kBThreads) {
+      const int64_t a = in_off[i], b = in_off[i + 1];
+      const int64_t len = b - a;
+      const int64_t q = len / 4, r = len % 4;
+      if (q == 0) continue;  // decided in phase 1
+      int64_t err = err_pos[i];
+      if (err == LLONG_MAX) err = -1;
+      if (err < 0 && r != 0) err = 4 * q;
+      if (err < 0) {
+        status[i] = B64_OK;
+        out_len[i] = out_off[i + 1] - out_off[i];
+      } else if (r != 0 && err == 4 * q) {
+        status[i] = B64_ERR_LENGTH;
+        out_len[i] = 3 * q;
+      } else {
+        status[i] = B64_ERR_INVALID_CHAR;
+        out_len[i] = 3 * (err / 4);
+      }
+      err_pos[i] = err;
+    }
+  }
 }
 
 }  // namespace b64

@@ -45,6 +45,13 @@ VARIANTS = {
     "w12_c1_in3": {"B64_WARPS_C": 12, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 3},
     "w24_c1_p2_in3": {"B64_WARPS_C": 24, "B64_CTAS_PER_SM": 1, "B64_SINGLE_PASSES": 2, "B64_STAGES_IN": 3},
     "skel_w16_c1_in3": {"B64_SKELETON": 1, "B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 3},
+    # batched (C2) variants
+    "b_plan_only": {"B64_BATCH_PLAN_ONLY": 1},
+    "b_p2": {"B64_BATCH_PASSES": 2},
+    "b_p8": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8},
+    "b_s8": {"B64_BATCH_SLOTS": 8, "B64_BATCH_WARPS": 8},
+    "b_w8": {"B64_BATCH_WARPS": 8},
+    "b_skel": {"B64_SKELETON": 1},
 }
 
 
@@ -68,7 +75,7 @@ def run(names, workload, steps, reps):
         for n in names:
             lib = os.path.join(OUT, f"libb64gpu_{n}.so")
             env = dict(os.environ, B64GPU_LIB=lib)
-            if "skel" in n:
+            if "skel" in n or "plan_only" in n:
                 env["B64_BENCH_NOCHECK"] = "1"
             cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", workload, "--steps", str(steps),
                    "--warmup", "3", "--no-e2e", "--no-cpu"]
@@ -79,13 +86,18 @@ def run(names, workload, steps, reps):
                 continue
             d = json.loads(line[-1])
             det = d["detail"]
-            row = {"variant": n, "rep": r, "value": d["value"], "enc_frac": det["encode_roofline_frac"],
-                   "dec_frac": det["decode_roofline_frac"], "sm_mhz": d["clocks"]["sm_mhz"],
-                   "reasons": d["clocks"]["reasons"]}
+            if "encode_roofline_frac" in det:
+                row = {"variant": n, "rep": r, "value": d["value"], "enc_frac": det["encode_roofline_frac"],
+                       "dec_frac": det["decode_roofline_frac"], "sm_mhz": d["clocks"]["sm_mhz"],
+                       "reasons": d["clocks"]["reasons"]}
+                print(f"{n:12} rep{r} value {d['value']:8.1f} GB/s  enc {det['encode_roofline_frac']:.3f} "
+                      f"dec {det['decode_roofline_frac']:.3f}  sm {d['clocks']['sm_mhz']} {d['clocks']['reasons']}",
+                      flush=True)
+            else:
+                row = {"variant": n, "rep": r, "value": d["value"], "detail": det}
+                short = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in det.items()}
+                print(f"{n:12} rep{r} value {d['value']:8.1f} GB/s  {short}", flush=True)
             rows.append(row)
-            print(f"{n:12} rep{r} value {d['value']:8.1f} GB/s  enc {det['encode_roofline_frac']:.3f} "
-                  f"dec {det['decode_roofline_frac']:.3f}  sm {d['clocks']['sm_mhz']} {d['clocks']['reasons']}",
-                  flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", f"sweep_{workload}.json"), "w") as f:
         json.dump(rows, f, indent=1)
