@@ -326,10 +326,16 @@ struct DevInfo {
 std::mutex g_mu;
 std::map<int, DevInfo> g_dev;
 
+constexpr int kMaxHostChunks = 256;
 struct StreamWs {
   DecWs *d_ws = nullptr;
   b64_result *h_res = nullptr;  // mapped pinned
   b64_result *d_res = nullptr;  // device alias of h_res
+  // host-buffer pipeline (created on first use)
+  bool pipe = false;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t e_in = nullptr, e_comp = nullptr, e_done = nullptr;
+  b64_result *h_chunks = nullptr, *d_chunks = nullptr;  // mapped, kMaxHostChunks records
 };
 std::map<std::pair<int, uintptr_t>, StreamWs> g_ws;
 
@@ -399,6 +405,30 @@ StreamWs *stream_ws(int dev, cudaStream_t stream) {
   if (cudaHostGetDevicePointer(&w.d_res, w.h_res, 0) != cudaSuccess) return nullptr;
   auto res = g_ws.emplace(key, w);
   return &res.first->second;
+}
+
+bool pipe_setup(StreamWs *w) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (w->pipe) return true;
+  if (cudaStreamCreateWithFlags(&w->s_in, cudaStreamNonBlocking) != cudaSuccess) return false;
+  if (cudaStreamCreateWithFlags(&w->s_out, cudaStreamNonBlocking) != cudaSuccess) return false;
+  for (cudaEvent_t *e : {&w->e_in, &w->e_comp, &w->e_done})
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return false;
+  if (cudaHostAlloc(&w->h_chunks, kMaxHostChunks * sizeof(b64_result), cudaHostAllocMapped) !=
+      cudaSuccess)
+    return false;
+  if (cudaHostGetDevicePointer(&w->d_chunks, w->h_chunks, 0) != cudaSuccess) return false;
+  w->pipe = true;
+  return true;
+}
+
+// Chunk size for the host pipeline: a multiple of `unit`, >= base, and at
+// most kMaxHostChunks chunks.
+int64_t host_chunk(int64_t total, int64_t base, int64_t unit) {
+  int64_t c = base;
+  const int64_t need = (total + kMaxHostChunks - 1) / kMaxHostChunks;
+  if (need > c) c = (need + unit - 1) / unit * unit;
+  return c;
 }
 
 int64_t grid_for(int64_t ntiles, int sms) {
@@ -563,18 +593,40 @@ int b64_decode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, in
                       d_status, d_ws, ws_bytes, stream, 1);
 }
 
+// Host-buffer entry points: the input is split into chunks; chunk i is
+// copied in on an internal stream, processed on `stream` as soon as it lands
+// and copied out on a second internal stream, so H2D, kernels and D2H of
+// different chunks overlap (PCIe / C2C full duplex).
 int64_t b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, uint8_t *d_scratch_in,
                         uint8_t *d_scratch_out, b64_stream_t stream) {
   if (n < 0 || (n > 0 && (!h_in || !h_out || !d_scratch_in || !d_scratch_out))) return B64_ERR_ARG;
   if (n == 0) return 0;
-  if (cudaMemcpyAsync(d_scratch_in, h_in, n, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  StreamWs *w = stream_ws(dev, stream);
+  if (w == nullptr || !pipe_setup(w)) return B64_ERR_CUDA;
+  const int64_t C = host_chunk(n, int64_t(48) << 20, 48);  // multiple of 3 and 16
+  for (int64_t off = 0; off < n; off += C) {
+    const int64_t len = n - off < C ? n - off : C;
+    const int64_t ooff = off / 3 * 4, olen = 4 * ((len + 2) / 3);
+    if (cudaMemcpyAsync(d_scratch_in + off, h_in + off, len, cudaMemcpyHostToDevice, w->s_in) !=
+            cudaSuccess ||
+        cudaEventRecord(w->e_in, w->s_in) != cudaSuccess ||
+        cudaStreamWaitEvent(stream, w->e_in, 0) != cudaSuccess)
+      return B64_ERR_CUDA;
+    const int64_t rc = b64_encode(d_scratch_in + off, len, d_scratch_out + ooff, stream);
+    if (rc < 0) return rc;
+    if (cudaEventRecord(w->e_comp, stream) != cudaSuccess ||
+        cudaStreamWaitEvent(w->s_out, w->e_comp, 0) != cudaSuccess ||
+        cudaMemcpyAsync(h_out + ooff, d_scratch_out + ooff, olen, cudaMemcpyDeviceToHost, w->s_out) !=
+            cudaSuccess)
+      return B64_ERR_CUDA;
+  }
+  if (cudaEventRecord(w->e_done, w->s_out) != cudaSuccess ||
+      cudaStreamWaitEvent(stream, w->e_done, 0) != cudaSuccess ||
+      cudaStreamSynchronize(stream) != cudaSuccess)
     return B64_ERR_CUDA;
-  const int64_t ol = b64_encode(d_scratch_in, n, d_scratch_out, stream);
-  if (ol < 0) return ol;
-  if (cudaMemcpyAsync(h_out, d_scratch_out, ol, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
-    return B64_ERR_CUDA;
-  if (cudaStreamSynchronize(stream) != cudaSuccess) return B64_ERR_CUDA;
-  return ol;
+  return 4 * ((n + 2) / 3);
 }
 
 int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out_len,
@@ -582,25 +634,57 @@ int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out
                     b64_stream_t stream) {
   if (m < 0 || (m > 0 && (!h_in || !d_scratch_in)) || (m >= 4 && (!h_out || !d_scratch_out)))
     return B64_ERR_ARG;
-  if (m > 0 &&
-      cudaMemcpyAsync(d_scratch_in, h_in, m, cudaMemcpyHostToDevice, stream) != cudaSuccess)
-    return B64_ERR_CUDA;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
-  if (w == nullptr) return B64_ERR_CUDA;
-  int rc = decode_launch(d_scratch_in, m, 1, d_scratch_out, w->d_res, stream, w->d_ws);
-  if (rc != B64_OK) return rc;
-  const int64_t cap = 3 * (m / 4);
-  if (cap > 0 &&
-      cudaMemcpyAsync(h_out, d_scratch_out, cap, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+  if (w == nullptr || !pipe_setup(w)) return B64_ERR_CUDA;
+  const int64_t C = host_chunk(m, int64_t(64) << 20, 64);  // multiple of 4 and 16
+  int nch = 0;
+  for (int64_t off = 0; off == 0 || off < m; off += C, ++nch) {
+    const int64_t len = m - off < C ? m - off : C;
+    const bool last = off + len >= m;
+    if (len > 0 && (cudaMemcpyAsync(d_scratch_in + off, h_in + off, len, cudaMemcpyHostToDevice,
+                                    w->s_in) != cudaSuccess ||
+                    cudaEventRecord(w->e_in, w->s_in) != cudaSuccess ||
+                    cudaStreamWaitEvent(stream, w->e_in, 0) != cudaSuccess))
+      return B64_ERR_CUDA;
+    const int64_t ooff = off / 4 * 3;
+    const int rc = decode_launch(d_scratch_in + off, len, last ? 1 : 0, d_scratch_out + ooff,
+                                 w->d_chunks + nch, stream, w->d_ws);
+    if (rc != B64_OK) return rc;
+    const int64_t cap = 3 * (len / 4);
+    if (cap > 0 && (cudaEventRecord(w->e_comp, stream) != cudaSuccess ||
+                    cudaStreamWaitEvent(w->s_out, w->e_comp, 0) != cudaSuccess ||
+                    cudaMemcpyAsync(h_out + ooff, d_scratch_out + ooff, cap,
+                                    cudaMemcpyDeviceToHost, w->s_out) != cudaSuccess))
+      return B64_ERR_CUDA;
+    if (last) {
+      ++nch;
+      break;
+    }
+  }
+  if (cudaEventRecord(w->e_done, w->s_out) != cudaSuccess ||
+      cudaStreamWaitEvent(stream, w->e_done, 0) != cudaSuccess ||
+      cudaStreamSynchronize(stream) != cudaSuccess)
     return B64_ERR_CUDA;
-  if (cudaStreamSynchronize(stream) != cudaSuccess) return B64_ERR_CUDA;
-  b64_result r;
-  std::memcpy(&r, w->h_res, sizeof(r));
-  if (out_len) *out_len = r.out_len;
-  if (err_pos) *err_pos = r.err_pos;
-  return r.status;
+  // Combine the chunk records: the first chunk with an error decides
+  // (chunks split on 4-character boundaries, R-shard).
+  int64_t total = 0;
+  for (int i = 0; i < nch; ++i) {
+    b64_result r;
+    std::memcpy(&r, w->h_chunks + i, sizeof(r));
+    const int64_t off = static_cast<int64_t>(i) * C;
+    if (r.status != B64_OK) {
+      const int64_t e = off + r.err_pos;
+      if (out_len) *out_len = r.status == B64_ERR_LENGTH ? off / 4 * 3 + r.out_len : 3 * (e / 4);
+      if (err_pos) *err_pos = e;
+      return r.status;
+    }
+    total += r.out_len;
+  }
+  if (out_len) *out_len = total;
+  if (err_pos) *err_pos = -1;
+  return B64_OK;
 }
 
 int b64_shard(int64_t total, int unit, int world, int rank, int64_t *begin, int64_t *end) {

@@ -408,3 +408,34 @@ def test_host_buffer_api():
     hy = torch.empty(b64.b64_decoded_max_len(n), dtype=torch.uint8).pin_memory()
     st, ol, ep = b64.b64_decode_host(ht, hy, so, si)
     assert (st, ep, ol) == (0, -1, x.size) and np.array_equal(hy.numpy()[:ol], x)
+
+
+def test_host_buffer_api_multichunk():
+    """Host pipeline over several 48 MiB / 64 MiB chunks: round trip, an
+    error in a middle chunk, '=' at a chunk seam, LENGTH on the last chunk."""
+    from tests import oracle_par
+
+    n = 150_000_001
+    x = splitmix_bytes(118, 0, n)
+    hx = torch.from_numpy(x).pin_memory()
+    m = b64.b64_encoded_len(n)
+    ht = torch.empty(m, dtype=torch.uint8).pin_memory()
+    si = torch.empty(m, dtype=torch.uint8, device=DEV)
+    so = torch.empty(m, dtype=torch.uint8, device=DEV)
+    assert b64.b64_encode_host(hx, ht, si, so) == m
+    ref = oracle_par.encode(x)
+    assert np.array_equal(ht.numpy(), ref)
+    hy = torch.empty(b64.b64_decoded_max_len(m), dtype=torch.uint8).pin_memory()
+    st, ol, ep = b64.b64_decode_host(ht, hy, si, so)
+    assert (st, ol, ep) == (0, n, -1) and np.array_equal(hy.numpy()[:n], x)
+    for pos, byte, cut in [(70_000_123, 0x21, 0), ((64 << 20) - 1, ord("="), 0), (0, None, 3)]:
+        t = ref.copy()
+        if byte is not None:
+            t[pos] = byte
+        if cut:
+            t = t[:-cut]
+        ht2 = torch.from_numpy(t).pin_memory()
+        st, ol, ep = b64.b64_decode_host(ht2, hy, si, so)
+        rst, rep, rout = oracle_par.decode(t)
+        assert (st, ep, ol) == (rst, rep, rout.size), (pos, st, ep, ol, rst, rep)
+        assert np.array_equal(hy.numpy()[:ol], rout)
