@@ -1,0 +1,25 @@
+#!/bin/bash
+# Round-end evidence on the GPU box: plain runs first (must exit 0), then
+#  * ncu --set full of encode_kernel / decode_kernel on C3 (one launch each)
+#  * ncu --set full of the batched kernels on C2
+#  * DRAM bytes of the C5 launches (single-pass metrics, no replay of 80 GB)
+#  * the launch list (gpu__time_duration) of the default bench command
+set -u
+T=${1:-r01}
+mkdir -p gpurun_out
+B3="python bench.py --workload c3 --steps 2 --warmup 3 --no-e2e --no-cpu"
+$B3 > gpurun_out/${T}_c3plain.json 2>&1 || { echo "c3 plain failed"; exit 1; }
+ncu --set full --clock-control none --import-source on -k regex:encode_kernel -s 3 -c 1 -o gpurun_out/${T}_enc_c3 -f $B3 > gpurun_out/${T}_ncu_enc.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 3 -c 1 -o gpurun_out/${T}_dec_c3 -f $B3 > gpurun_out/${T}_ncu_dec.log 2>&1
+B2="python bench.py --workload c2 --steps 1 --warmup 3"
+$B2 > gpurun_out/${T}_c2plain.json 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:batch_kernel -s 4 -c 2 -o gpurun_out/${T}_batch_c2 -f $B2 > gpurun_out/${T}_ncu_c2.log 2>&1
+B5="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu"
+$B5 > gpurun_out/${T}_c5plain.json 2>&1 && \
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:"(en|de)code_kernel" -s 6 -c 2 --csv --log-file gpurun_out/${T}_c5_traffic.csv $B5 > /dev/null 2>&1
+D="python bench.py"
+$D > gpurun_out/${T}_bench_plain.json 2> gpurun_out/${T}_bench_plain.err && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/${T}_launches.csv $D > gpurun_out/${T}_ncu_launch.log 2>&1
+echo profile-all-done
