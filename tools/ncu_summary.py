@@ -36,7 +36,45 @@ def main():
     rep = sys.argv[1]
     algo = float(sys.argv[2]) if len(sys.argv) > 2 else None
     rows = list(csv.reader(io.StringIO(run([rep, "--page", "raw", "--csv"]))))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    outs = [summarize(rep, hdr, units, vals, algo) for vals in rows[2:]]
+    src = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
+    # the source page holds one table per profiled kernel, in launch order
+    tables, cur = [], None
+    for r in src:
+        if r and r[0] == "Kernel Name":
+            cur = {"rows": []}
+            tables.append(cur)
+        elif r and r[0] == "Address" and cur is not None:
+            cur["hdr"] = r
+        elif cur is not None and "hdr" in cur:
+            cur["rows"].append(r)
+    for out, t in zip(outs, tables):
+        add_mix(out, t)
+    json.dump(outs if len(outs) > 1 else outs[0], sys.stdout, indent=1)
+    print()
+
+
+def add_mix(out, t):
+    ix = {k: i for i, k in enumerate(t["hdr"])}
+    mix = Counter()
+    total = 0
+    for r in t["rows"]:
+        try:
+            ie = int(r[ix["Instructions Executed"]] or 0)
+        except (ValueError, IndexError):
+            continue
+        total += ie
+        toks = r[ix["Source"]].strip().split()
+        if not toks:
+            continue
+        op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+        mix[op.split(".")[0]] += ie
+    out["warp_instructions"] = total
+    out["opcode_mix_top"] = dict(mix.most_common(16))
+
+
+def summarize(rep, hdr, units, vals, algo):
     kernel = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
     out = {"report": rep, "kernel": kernel}
     for k in KEYS:
@@ -60,27 +98,7 @@ def main():
             out["traffic_over_algorithmic"] = (rd + wr) / algo
     except (KeyError, ValueError):
         pass
-    src = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
-    if len(src) > 2:
-        h = src[1]
-        ix = {k: i for i, k in enumerate(h)}
-        mix = Counter()
-        total = 0
-        for r in src[2:]:
-            try:
-                ie = int(r[ix["Instructions Executed"]] or 0)
-            except (ValueError, IndexError):
-                continue
-            total += ie
-            toks = r[ix["Source"]].strip().split()
-            if not toks:
-                continue
-            op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
-            mix[op.split(".")[0]] += ie
-        out["warp_instructions"] = total
-        out["opcode_mix_top"] = dict(mix.most_common(16))
-    json.dump(out, sys.stdout, indent=1)
-    print()
+    return out
 
 
 if __name__ == "__main__":
