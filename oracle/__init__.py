@@ -24,7 +24,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "b64_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-OK, INVALID_CHAR, LENGTH = 0, 1, 2
+OK, INVALID_CHAR, LENGTH, NONCANONICAL = 0, 1, 2, 3
+URL, NOPAD, STRICT = 1, 2, 4
 
 _lib = None
 _lock = threading.Lock()
@@ -58,6 +59,18 @@ def _load():
                                           ctypes.POINTER(ctypes.c_int64),
                                           ctypes.POINTER(ctypes.c_int64)]
             lib.oracle_decode.restype = ctypes.c_int
+            lib.oracle_B_ex.argtypes = [ctypes.c_int, ctypes.c_int]
+            lib.oracle_B_ex.restype = ctypes.c_int
+            lib.oracle_A_ex.argtypes = [ctypes.c_int, ctypes.c_int]
+            lib.oracle_A_ex.restype = ctypes.c_int
+            lib.oracle_encoded_len_ex.argtypes = [ctypes.c_int64, ctypes.c_int]
+            lib.oracle_encoded_len_ex.restype = ctypes.c_int64
+            lib.oracle_encode_ex.argtypes = [u8p, ctypes.c_int64, u8p, ctypes.c_int]
+            lib.oracle_encode_ex.restype = ctypes.c_int64
+            lib.oracle_decode_ex.argtypes = [u8p, ctypes.c_int64, u8p,
+                                             ctypes.POINTER(ctypes.c_int64),
+                                             ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+            lib.oracle_decode_ex.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -135,3 +148,34 @@ def decode_batch(text: np.ndarray, off: np.ndarray):
 
 def encode_batch(raw: np.ndarray, off: np.ndarray):
     return [encode(raw[off[i]: off[i + 1]]) for i in range(off.size - 1)]
+
+
+def B_ex(v: int, flags: int) -> int:
+    return _load().oracle_B_ex(int(v), int(flags))
+
+
+def A_ex(ch: int, flags: int) -> int:
+    return _load().oracle_A_ex(int(ch), int(flags))
+
+
+def encode_ex(s, flags: int) -> np.ndarray:
+    """Algorithm 1 variants (base64url / unpadded), SURVEY §8(f) f1."""
+    a = _as_u8(s)
+    lib = _load()
+    out = np.empty(lib.oracle_encoded_len_ex(a.size, flags), dtype=np.uint8)
+    w = lib.oracle_encode_ex(a.ctypes.data if a.size else None, a.size,
+                             out.ctypes.data if out.size else None, flags)
+    assert w == out.size
+    return out
+
+
+def decode_ex(c, flags: int):
+    """Algorithm 2 variants (base64url, optional padding, App. A strict)."""
+    a = _as_u8(c)
+    lib = _load()
+    out = np.empty(3 * (a.size // 4) + 3, dtype=np.uint8)
+    ol = ctypes.c_int64(0)
+    ep = ctypes.c_int64(0)
+    st = lib.oracle_decode_ex(a.ctypes.data if a.size else None, a.size, out.ctypes.data,
+                              ctypes.byref(ol), ctypes.byref(ep), flags)
+    return int(st), int(ep.value), out[: ol.value].copy()

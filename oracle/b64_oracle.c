@@ -136,3 +136,162 @@ int oracle_decode(const uint8_t *c, int64_t m, uint8_t *p, int64_t *out_len,
   }
   return ORACLE_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * Variants.  Flags:
+ *   ORACLE_URL    base64url alphabet: 62 -> '-', 63 -> '_'
+ *   ORACLE_NOPAD  encode omits '=' ("it may be acceptable to omit the
+ *                 padding characters if the size ... is otherwise known");
+ *                 decode accepts a final partial quad of 2 or 3 characters
+ *                 as if padded (padding optional; padded input still valid)
+ *   ORACLE_STRICT Appendix A: the trailing bits of the final
+ *                 quad must be zero (status ORACLE_NONCANONICAL at the
+ *                 offending character), checked after an otherwise
+ *                 successful decode.
+ * ------------------------------------------------------------------------ */
+#define ORACLE_URL 1
+#define ORACLE_NOPAD 2
+#define ORACLE_STRICT 4
+#define ORACLE_NONCANONICAL 3
+
+int oracle_B_ex(int v, int flags) {
+  if (flags & ORACLE_URL) {
+    if (v == 62) return '-';
+    if (v == 63) return '_';
+  }
+  return oracle_B(v);
+}
+
+int oracle_A_ex(int ch, int flags) {
+  if (flags & ORACLE_URL) {
+    if (ch == '-') return 62;
+    if (ch == '_') return 63;
+    if (ch == '+' || ch == '/') return -1;
+  }
+  return oracle_A(ch);
+}
+
+int64_t oracle_encoded_len_ex(int64_t n, int flags) {
+  if (flags & ORACLE_NOPAD) return 4 * (n / 3) + (n % 3 ? n % 3 + 1 : 0);
+  return oracle_encoded_len(n);
+}
+
+/* Algorithm 1 with the variant alphabet; NOPAD drops the '='
+ * appended at P:141 and P:146. */
+int64_t oracle_encode_ex(const uint8_t *s, int64_t n, uint8_t *p, int flags) {
+  int64_t o = 0;
+  int64_t i;
+  for (i = 0; i + 3 <= n - (n % 3); i += 3) {
+    p[o++] = (uint8_t)oracle_B_ex(s[i] / 4, flags);
+    p[o++] = (uint8_t)oracle_B_ex(((s[i] * 16) % 64) + (s[i + 1] / 16), flags);
+    p[o++] = (uint8_t)oracle_B_ex(((s[i + 1] * 4) % 64) + (s[i + 2] / 64), flags);
+    p[o++] = (uint8_t)oracle_B_ex(s[i + 2] % 64, flags);
+  }
+  i = n - n % 3;
+  if (i < n) {
+    p[o++] = (uint8_t)oracle_B_ex(s[i] / 4, flags);
+    if (i == n - 1) {
+      p[o++] = (uint8_t)oracle_B_ex((s[i] * 16) % 64, flags);
+      if (!(flags & ORACLE_NOPAD)) p[o++] = '=';
+    } else if (i == n - 2) {
+      p[o++] = (uint8_t)oracle_B_ex(((s[i] * 16) % 64) + (s[i + 1] / 16), flags);
+      p[o++] = (uint8_t)oracle_B_ex((s[i + 1] * 4) % 64, flags);
+    }
+    if (!(flags & ORACLE_NOPAD)) p[o++] = '=';
+  }
+  return o;
+}
+
+static int acceptable_ex(const uint8_t *c, int64_t m, int64_t i, int flags) {
+  const int in_alphabet = oracle_A_ex(c[i], flags) >= 0;
+  if (m % 4 == 0 && i == m - 1)
+    return (in_alphabet || c[i] == '=') && (c[m - 2] != '=' || c[i] == '=');
+  if (m % 4 == 0 && i == m - 2) return in_alphabet || c[i] == '=';
+  return in_alphabet;
+}
+
+/* Algorithm 2 with the variant alphabet, optional padding and
+ * the Appendix A check.  p must hold 3*floor(m/4) + 2 bytes. */
+int oracle_decode_ex(const uint8_t *c, int64_t m, uint8_t *p, int64_t *out_len, int64_t *err_pos,
+                     int flags) {
+  int64_t o = 0;
+  const int64_t q = m / 4;
+  const int64_t r = m % 4;
+  int64_t i;
+  int64_t last_data = -1; /* position whose trailing bits App. A constrains */
+  int64_t last_shift = 0; /* 16 (two pads) or 64 (one pad) */
+  *err_pos = -1;
+  for (i = 0; i + 4 <= 4 * q; i += 4) {
+    int j;
+    int a, b, cc, d;
+    for (j = 0; j < 4; ++j) {
+      if (!acceptable_ex(c, m, i + j, flags)) {
+        *err_pos = i + j;
+        *out_len = o;
+        return ORACLE_INVALID_CHAR;
+      }
+    }
+    a = c[i] == '=' ? 0 : oracle_A_ex(c[i], flags);
+    b = c[i + 1] == '=' ? 0 : oracle_A_ex(c[i + 1], flags);
+    cc = c[i + 2] == '=' ? 0 : oracle_A_ex(c[i + 2], flags);
+    d = c[i + 3] == '=' ? 0 : oracle_A_ex(c[i + 3], flags);
+    p[o++] = (uint8_t)((a * 4) + (b / 16));
+    if (c[i + 2] == '=') {
+      last_data = i + 1;
+      last_shift = 16;
+      break;
+    }
+    p[o++] = (uint8_t)(((b * 16) % 256) + (cc / 4));
+    if (c[i + 3] == '=') {
+      last_data = i + 2;
+      last_shift = 64;
+      break;
+    }
+    p[o++] = (uint8_t)(((cc * 64) % 256) + d);
+  }
+  if (r != 0) {
+    if (!(flags & ORACLE_NOPAD) || r == 1) { /* R-length */
+      *out_len = o;
+      *err_pos = 4 * q;
+      return ORACLE_LENGTH;
+    }
+    /* NOPAD: the partial final quad, decoded as if padded.
+     * Its characters must be data; a '=' in its third position can still
+     * continue a padded quad ("xx=" -> "xx=="), so that input is merely
+     * truncated: LENGTH at 4q (reading R2 / R-length). */
+    for (i = 4 * q; i < m; ++i) {
+      if (oracle_A_ex(c[i], flags) < 0) {
+        *out_len = o;
+        if (i == 4 * q + 2 && c[i] == '=') {
+          *err_pos = 4 * q;
+          return ORACLE_LENGTH;
+        }
+        *err_pos = i;
+        return ORACLE_INVALID_CHAR;
+      }
+    }
+    {
+      const int a = oracle_A_ex(c[4 * q], flags);
+      const int b = oracle_A_ex(c[4 * q + 1], flags);
+      p[o++] = (uint8_t)((a * 4) + (b / 16));
+      last_data = 4 * q + 1;
+      last_shift = 16;
+      if (r == 3) {
+        const int cc = oracle_A_ex(c[4 * q + 2], flags);
+        p[o++] = (uint8_t)(((b * 16) % 256) + (cc / 4));
+        last_data = 4 * q + 2;
+        last_shift = 64;
+      }
+    }
+  }
+  *out_len = o;
+  /* Appendix A: (A(C_{n-3}) x 16) mod 256 = 0 with two pads,
+   * (A(C_{n-2}) x 64) mod 256 = 0 with one pad. */
+  if ((flags & ORACLE_STRICT) && last_data >= 0 &&
+      (oracle_A_ex(c[last_data], flags) * last_shift) % 256 != 0) {
+    *err_pos = last_data;
+    *out_len = 3 * (last_data / 4);
+    return ORACLE_NONCANONICAL;
+  }
+  return ORACLE_OK;
+}
