@@ -44,10 +44,21 @@ typedef enum {
   B64_OK = 0,               /* valid input, fully decoded                            */
   B64_ERR_INVALID_CHAR = 1, /* a byte outside the alphabet / misplaced '=' */
   B64_ERR_LENGTH = 2,       /* m not divisible by 4 (Alg 2 requires it)        */
+  B64_ERR_NONCANONICAL = 3, /* B64_FLAG_STRICT: non-zero trailing bits (App. A) */
   B64_ERR_ARG = -1,         /* bad argument; nothing launched                          */
   B64_ERR_CUDA = -2,        /* a CUDA runtime call failed                              */
   B64_ERR_WORKSPACE = -3    /* batched workspace too small                             */
 } b64_status;
+
+/* Variant flags; 0 = the paper's default
+ * (standard alphabet, '=' padding required, non-canonical bits accepted). */
+enum {
+  B64_FLAG_URL = 1,    /* base64url alphabet: 62 -> '-', 63 -> '_'               */
+  B64_FLAG_NOPAD = 2,  /* encode: no '='; decode: padding optional, a final partial
+                          quad of 2 or 3 characters decodes as if padded        */
+  B64_FLAG_STRICT = 4  /* decode: reject non-zero trailing bits of the final quad
+                          (Appendix A) with B64_ERR_NONCANONICAL at that character      */
+};
 
 /* Device-side result record of one decode (16-byte aligned). */
 typedef struct {
@@ -67,6 +78,12 @@ int64_t b64_encoded_len(int64_t n);
  * (Alg 2 emits at most 3 bytes per complete quad). -1 if m < 0. */
 int64_t b64_decoded_max_len(int64_t m);
 
+/* Variant sizes: encoded length under `flags` (NOPAD: ceil(4n/3)); decode
+ * output capacity under `flags` (NOPAD adds r-1 bytes for an r = 2, 3
+ * character tail).  -1 on a bad argument. */
+int64_t b64_encoded_len_ex(int64_t n, int flags);
+int64_t b64_decoded_max_len_ex(int64_t m, int flags);
+
 /* ----------------------------------------------------------------- encode */
 
 /* Algorithm 1 on n bytes at d_in: writes exactly
@@ -74,6 +91,11 @@ int64_t b64_decoded_max_len(int64_t m);
  * to d_out, '=' padded, no line breaks.  Asynchronous on `stream`.
  * Returns the output length, or B64_ERR_ARG / B64_ERR_CUDA. */
 int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t stream);
+
+/* b64_encode with variant flags (B64_FLAG_URL, B64_FLAG_NOPAD; STRICT is
+ * ignored): writes b64_encoded_len_ex(n, flags) characters. */
+int64_t b64_encode_ex(const uint8_t *d_in, int64_t n, uint8_t *d_out, int flags,
+                      b64_stream_t stream);
 
 /* ----------------------------------------------------------------- decode */
 
@@ -98,6 +120,15 @@ int b64_decode(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *out_len,
  * aligned) when the kernel finishes.  Returns B64_OK if enqueued. */
 int b64_decode_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, b64_result *d_result,
                      b64_stream_t stream);
+
+/* Decode with variant flags (URL alphabet, optional padding, strict
+ * trailing bits).  d_out capacity: b64_decoded_max_len_ex(m, flags).  Status
+ * and offsets as b64_decode, plus B64_ERR_NONCANONICAL (err_pos = the
+ * character whose low bits are non-zero, out_len = 3*floor(err_pos/4)). */
+int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int64_t *out_len,
+                  int64_t *err_pos, b64_stream_t stream);
+int b64_decode_ex_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
+                        b64_result *d_result, b64_stream_t stream);
 
 /* Decode of one shard of a larger buffer split on 4-character boundaries
  * (multi-GPU sharder).  final_shard != 0: identical to
@@ -136,6 +167,16 @@ int b64_encode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, in
 int b64_decode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
                      uint8_t *d_out, int64_t *d_out_off, int64_t *d_out_len, int64_t *d_err_pos,
                      int32_t *d_status, void *d_ws, size_t ws_bytes, b64_stream_t stream);
+
+/* Batched variants with flags (per-message semantics of b64_encode_ex /
+ * b64_decode_ex; output reservations use the variant sizes). */
+int b64_encode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                        uint8_t *d_out, int64_t *d_out_off, int flags, void *d_ws, size_t ws_bytes,
+                        b64_stream_t stream);
+int b64_decode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                        uint8_t *d_out, int64_t *d_out_off, int64_t *d_out_len, int64_t *d_err_pos,
+                        int32_t *d_status, int flags, void *d_ws, size_t ws_bytes,
+                        b64_stream_t stream);
 
 /* ------------------------------------------------------------ host buffers */
 

@@ -14,6 +14,15 @@ from ._lib import (  # noqa: F401
     B64_ERR_CUDA,
     B64_ERR_INVALID_CHAR,
     B64_ERR_LENGTH,
+    B64_ERR_NONCANONICAL,
+    B64_FLAG_NOPAD,
+    B64_FLAG_STRICT,
+    B64_FLAG_URL,
+    b64_decode_ex,
+    b64_decode_ex_async,
+    b64_decoded_max_len_ex,
+    b64_encode_ex,
+    b64_encoded_len_ex,
     B64_ERR_WORKSPACE,
     B64_OK,
     B64Error,

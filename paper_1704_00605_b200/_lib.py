@@ -17,6 +17,10 @@ if os.environ.get("B64GPU_LIB"):
 B64_OK = 0
 B64_ERR_INVALID_CHAR = 1
 B64_ERR_LENGTH = 2
+B64_ERR_NONCANONICAL = 3
+B64_FLAG_URL = 1
+B64_FLAG_NOPAD = 2
+B64_FLAG_STRICT = 4
 B64_ERR_ARG = -1
 B64_ERR_CUDA = -2
 B64_ERR_WORKSPACE = -3
@@ -27,6 +31,8 @@ EXPORTS = (
     "b64_decode_async", "b64_decode_shard_async", "b64_batch_workspace_bytes",
     "b64_encode_batch", "b64_decode_batch", "b64_encode_host", "b64_decode_host",
     "b64_shard", "b64_status_str", "b64_build_info",
+    "b64_encoded_len_ex", "b64_decoded_max_len_ex", "b64_encode_ex", "b64_decode_ex",
+    "b64_decode_ex_async", "b64_encode_batch_ex", "b64_decode_batch_ex",
 )
 
 _lib = None
@@ -72,6 +78,13 @@ def load_library():
         "b64_shard": (i32, [i64, i32, i32, i32, p64, p64]),
         "b64_status_str": (ctypes.c_char_p, [i32]),
         "b64_build_info": (ctypes.c_char_p, []),
+        "b64_encoded_len_ex": (i64, [i64, i32]),
+        "b64_decoded_max_len_ex": (i64, [i64, i32]),
+        "b64_encode_ex": (i64, [vp, i64, vp, i32, vp]),
+        "b64_decode_ex": (i32, [vp, i64, vp, i32, p64, p64, vp]),
+        "b64_decode_ex_async": (i32, [vp, i64, vp, i32, vp, vp]),
+        "b64_encode_batch_ex": (i32, [vp, vp, i64, i64, vp, vp, i32, vp, sz, vp]),
+        "b64_decode_batch_ex": (i32, [vp, vp, i64, i64, vp, vp, vp, vp, vp, i32, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -122,29 +135,40 @@ def b64_build_info() -> str:
 
 # -------------------------------------------------------------- encode ---
 
-def b64_encode(inp, out=None, stream=None):
+def b64_encoded_len_ex(n: int, flags: int) -> int:
+    return load_library().b64_encoded_len_ex(n, flags)
+
+
+def b64_decoded_max_len_ex(m: int, flags: int) -> int:
+    return load_library().b64_decoded_max_len_ex(m, flags)
+
+
+def b64_encode(inp, out=None, stream=None, flags: int = 0):
     """Encode the uint8 CUDA tensor ``inp``; returns the output view."""
     import torch
 
     _check_u8_cuda(inp, "inp")
     lib = load_library()
     n = inp.numel()
-    need = lib.b64_encoded_len(n)
+    need = lib.b64_encoded_len_ex(n, flags)
     if out is None:
         out = torch.empty(max(need, 1), dtype=torch.uint8, device=inp.device)
     else:
         _check_u8_cuda(out, "out")
         if out.numel() < need:
             raise ValueError("out too small")
-    rc = lib.b64_encode(_ptr(inp), n, _ptr(out), _stream(stream, inp.device))
+    rc = lib.b64_encode_ex(_ptr(inp), n, _ptr(out), flags, _stream(stream, inp.device))
     if rc < 0:
         raise B64Error(rc, "b64_encode")
     return out[:rc]
 
 
+b64_encode_ex = b64_encode
+
+
 # -------------------------------------------------------------- decode ---
 
-def b64_decode(inp, out=None, stream=None):
+def b64_decode(inp, out=None, stream=None, flags: int = 0):
     """Validating decode (synchronizes the stream).
 
     Returns (out_view, status, err_pos); out_view has out_len bytes."""
@@ -153,7 +177,7 @@ def b64_decode(inp, out=None, stream=None):
     _check_u8_cuda(inp, "inp")
     lib = load_library()
     m = inp.numel()
-    cap = lib.b64_decoded_max_len(m)
+    cap = lib.b64_decoded_max_len_ex(m, flags)
     if out is None:
         out = torch.empty(max(cap, 1), dtype=torch.uint8, device=inp.device)
     else:
@@ -162,11 +186,14 @@ def b64_decode(inp, out=None, stream=None):
             raise ValueError("out too small")
     ol = ctypes.c_int64(0)
     ep = ctypes.c_int64(0)
-    st = lib.b64_decode(_ptr(inp), m, _ptr(out), ctypes.byref(ol), ctypes.byref(ep),
-                        _stream(stream, inp.device))
+    st = lib.b64_decode_ex(_ptr(inp), m, _ptr(out), flags, ctypes.byref(ol), ctypes.byref(ep),
+                           _stream(stream, inp.device))
     if st < 0:
         raise B64Error(st, "b64_decode")
     return out[: ol.value], st, ep.value
+
+
+b64_decode_ex = b64_decode
 
 
 def result_tensor(device):
@@ -184,8 +211,18 @@ def unpack_result(res):
     return v[0], v[1], st, pc
 
 
-def b64_decode_async(inp, out, result, stream=None):
+def b64_decode_async(inp, out, result, stream=None, flags: int = 0):
+    if flags:
+        return b64_decode_ex_async(inp, out, result, flags, stream)
     return b64_decode_shard_async(inp, out, result, final_shard=True, stream=stream)
+
+
+def b64_decode_ex_async(inp, out, result, flags: int, stream=None):
+    lib = load_library()
+    rc = lib.b64_decode_ex_async(_ptr(inp), inp.numel(), _ptr(out), flags, result.data_ptr(),
+                                 _stream(stream, inp.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_decode_ex_async")
 
 
 def b64_decode_shard_async(inp, out, result, final_shard=True, stream=None):
@@ -222,7 +259,8 @@ def _ws(k, total, direction, device, ws):
     return ws[off:], need
 
 
-def b64_encode_batch(inp, in_off, out=None, out_off=None, ws=None, total_in=None, stream=None):
+def b64_encode_batch(inp, in_off, out=None, out_off=None, ws=None, total_in=None, stream=None,
+                     flags: int = 0):
     """Batched encode; in_off: int64[k+1] CUDA tensor.  Returns (out, out_off)."""
     import torch
 
@@ -234,16 +272,16 @@ def b64_encode_batch(inp, in_off, out=None, out_off=None, ws=None, total_in=None
     if out_off is None:
         out_off = torch.empty(k + 1, dtype=torch.int64, device=inp.device)
     w, need = _ws(k, total, 0, inp.device, ws)
-    rc = load_library().b64_encode_batch(_ptr(inp), in_off.data_ptr(), k, total, _ptr(out),
-                                         out_off.data_ptr(), w.data_ptr(), w.numel(),
-                                         _stream(stream, inp.device))
+    rc = load_library().b64_encode_batch_ex(_ptr(inp), in_off.data_ptr(), k, total, _ptr(out),
+                                            out_off.data_ptr(), flags, w.data_ptr(), w.numel(),
+                                            _stream(stream, inp.device))
     if rc < 0:
         raise B64Error(rc, "b64_encode_batch")
     return out, out_off
 
 
 def b64_decode_batch(inp, in_off, out=None, out_off=None, out_len=None, err_pos=None,
-                     status=None, ws=None, total_in=None, stream=None):
+                     status=None, ws=None, total_in=None, stream=None, flags: int = 0):
     """Batched validating decode.  Returns (out, out_off, out_len, err_pos, status)."""
     import torch
 
@@ -252,7 +290,7 @@ def b64_decode_batch(inp, in_off, out=None, out_off=None, out_len=None, err_pos=
     dev = inp.device
     total = inp.numel() if total_in is None else total_in
     if out is None:
-        out = torch.empty(max(3 * (total // 4) + 1, 1), dtype=torch.uint8, device=dev)
+        out = torch.empty(max(3 * (total // 4) + 2 * k + 1, 1), dtype=torch.uint8, device=dev)
     if out_off is None:
         out_off = torch.empty(k + 1, dtype=torch.int64, device=dev)
     if out_len is None:
@@ -262,10 +300,10 @@ def b64_decode_batch(inp, in_off, out=None, out_off=None, out_len=None, err_pos=
     if status is None:
         status = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
     w, need = _ws(k, total, 1, dev, ws)
-    rc = load_library().b64_decode_batch(_ptr(inp), in_off.data_ptr(), k, total, _ptr(out),
-                                         out_off.data_ptr(), out_len.data_ptr(), err_pos.data_ptr(),
-                                         status.data_ptr(), w.data_ptr(), w.numel(),
-                                         _stream(stream, dev))
+    rc = load_library().b64_decode_batch_ex(_ptr(inp), in_off.data_ptr(), k, total, _ptr(out),
+                                            out_off.data_ptr(), out_len.data_ptr(),
+                                            err_pos.data_ptr(), status.data_ptr(), flags,
+                                            w.data_ptr(), w.numel(), _stream(stream, dev))
     if rc < 0:
         raise B64Error(rc, "b64_decode_batch")
     return out, out_off, out_len[:k], err_pos[:k], status[:k]

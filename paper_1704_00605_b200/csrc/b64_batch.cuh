@@ -135,16 +135,16 @@ __device__ __forceinline__ void block_exclusive_scan2(int64_t a, int64_t b, int6
 // Output size and unit count of message [a, b) (decode: reads the pads).
 template <bool DECODE>
 __device__ __forceinline__ void msg_sizes(const uint8_t *in, int64_t a, int64_t b, int64_t &osz,
-                                          int64_t &units) {
+                                          int64_t &units, int flags) {
   const int64_t len = b - a;
   if (DECODE) {
-    const int64_t q = len / 4;
+    const int64_t q = len / 4, r = len & 3;
     int64_t p = 0;
-    if ((len & 3) == 0 && q > 0 && in[b - 1] == '=') p = (in[b - 2] == '=') ? 2 : 1;
-    osz = 3 * q - p;
+    if (r == 0 && q > 0 && in[b - 1] == '=') p = (in[b - 2] == '=') ? 2 : 1;
+    osz = 3 * q - p + (((flags & kFlagNoPad) && r >= 2) ? r - 1 : 0);
     units = (4 * q + DU::kIn - 1) / DU::kIn;
   } else {
-    osz = 4 * ((len + 2) / 3);
+    osz = enc_len(len, flags);
     units = (len + EU::kIn - 1) / EU::kIn;
   }
 }
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
                  const int64_t *__restrict__ in_off, int64_t *__restrict__ out_off,
                  int64_t *__restrict__ unit_off, int64_t *__restrict__ blk,
                  int64_t *__restrict__ err_pos, int64_t *__restrict__ out_len,
-                 int32_t *__restrict__ status, unsigned int *__restrict__ msg_done) {
+                 int32_t *__restrict__ status, unsigned int *__restrict__ msg_done, int flags) {
   using Ring = typename std::conditional<DECODE, DecRing, EncRing>::type;
   constexpr int UIN = DECODE ? DU::kIn : EU::kIn;
   constexpr int UOUT = DECODE ? DU::kOut : EU::kOut;
@@ -273,10 +273,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
   if (DECODE) {
     if (tid < 256) g_dec_tab[tid] = kInvalid;
     __syncthreads();
-    if (tid < 64) g_dec_tab[ascii_of(tid)] = static_cast<uint8_t>(tid);
+    if (tid < 64) g_dec_tab[ascii_of(tid, flags)] = static_cast<uint8_t>(tid);
   } else {
-    if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid));
+    if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid, flags));
   }
+  const bool pad = !(flags & kFlagNoPad);
   if (lane == 0) {
     for (int s = 0; s < kBSlots; ++s) mbar_init(&R.full[s], 1);
     fence_mbar_init();
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   for (int64_t r0 = i_lo; r0 < i_hi; r0 += kBThreads) {
     const int64_t i = r0 + tid;
     int64_t o = 0, u = 0;
-    if (i < i_hi) msg_sizes<DECODE>(in, in_off[i], in_off[i + 1], o, u);
+    if (i < i_hi) msg_sizes<DECODE>(in, in_off[i], in_off[i + 1], o, u, flags);
     int64_t po, pu, to, tu;
     block_exclusive_scan2(o, u, po, pu, to, tu, sh);
     tot_o += to;
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     if (i < i_hi) {
       a = in_off[i];
       b = in_off[i + 1];
-      msg_sizes<DECODE>(in, a, b, o, u);
+      msg_sizes<DECODE>(in, a, b, o, u, flags);
     }
     int64_t po, pu, to, tu;
     block_exclusive_scan2(o, u, po, pu, to, tu, sh);
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       unit_off[i] = bu + pu;
       if (DECODE) {
         const int64_t len = b - a;
-        if (u == 0) {  // no complete quad: the result is decided here
+        if (u == 0) {  // no complete quad: decided here (NOPAD 2-3 char tails: phase 3)
           status[i] = (len & 3) ? B64_ERR_LENGTH : B64_OK;
           err_pos[i] = (len & 3) ? 0 : -1;
           out_len[i] = 0;
@@ -436,16 +437,18 @@ __global__ void __launch_bounds__(kBThreads, 1)
     uint32_t werr = 0xFFFFFFFFu;
     if constexpr (!DECODE) {
       if (!congruent) {  // destination not 4-byte aligned: aligned stream + realigning copy
-        encode_tile<1, 16, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+        encode_tile<1, 16, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane, nullptr,
+                                                           pad);
       } else if (d.len == UIN) {
         if (in4)
           encode_tile<4, 4, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
         else
           encode_tile<1, 4, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
       } else {
-        encode_tile<1, 4, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+        encode_tile<1, 4, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane, nullptr,
+                                                          pad);
       }
-      olen = 4 * ((d.len + 2) / 3);
+      olen = static_cast<int>(enc_len(d.len, flags));
     } else {
       const bool fin = (d.flags & kFlagFinal) != 0;
       uint32_t ch1 = 0, ch2 = 0;
@@ -500,22 +503,13 @@ __global__ void __launch_bounds__(kBThreads, 1)
          i += static_cast<int64_t>(gridDim.x) * kBThreads) {
       const int64_t a = in_off[i], b = in_off[i + 1];
       const int64_t len = b - a;
-      const int64_t q = len / 4, r = len % 4;
-      if (q == 0) continue;  // decided in phase 1
-      int64_t err = err_pos[i];
+      if (len / 4 == 0 && !((flags & kFlagNoPad) && len >= 2)) continue;  // decided in phase 1
+      int64_t err = len / 4 == 0 ? LLONG_MAX : err_pos[i];
       if (err == LLONG_MAX) err = -1;
-      if (err < 0 && r != 0) err = 4 * q;
-      if (err < 0) {
-        status[i] = B64_OK;
-        out_len[i] = out_off[i + 1] - out_off[i];
-      } else if (r != 0 && err == 4 * q) {
-        status[i] = B64_ERR_LENGTH;
-        out_len[i] = 3 * q;
-      } else {
-        status[i] = B64_ERR_INVALID_CHAR;
-        out_len[i] = 3 * (err / 4);
-      }
-      err_pos[i] = err;
+      const StreamResult R = finish_stream(in + a, len, out + out_off[i], err, true, flags);
+      status[i] = R.status;
+      out_len[i] = R.out_len;
+      err_pos[i] = R.err_pos;
     }
   }
 }

@@ -85,8 +85,15 @@ struct TileDesc {
 static_assert(sizeof(TileDesc) == 40, "TileDesc layout");
 
 // ------------------------------------------------------- alphabet (GPU) ---
-// Table II: 6-bit value -> ASCII by range offsets.
-__device__ __forceinline__ uint32_t ascii_of(uint32_t v) {
+// Variant flags (include/b64gpu.h B64_FLAG_*).
+constexpr int kFlagUrl = 1;     // base64url alphabet
+constexpr int kFlagNoPad = 2;   // no '=' on encode, optional padding on decode
+constexpr int kFlagStrict = 4;  // Appendix A canonical trailing bits
+
+// Table II: 6-bit value -> ASCII by range offsets; base64url
+// moves 62 / 63 to '-' / '_'.
+__device__ __forceinline__ uint32_t ascii_of(uint32_t v, int flags = 0) {
+  if ((flags & kFlagUrl) && v >= 62) return v == 62 ? '-' : '_';
   int off = v < 26 ? 65 : v < 52 ? 71 : v < 62 ? -4 : v == 62 ? -19 : -16;
   return static_cast<uint32_t>(static_cast<int>(v) + off);
 }
@@ -233,7 +240,7 @@ __device__ __forceinline__ void set_byte16(uint32_t (&c)[4], int i, uint32_t v) 
 // (512 contiguous bytes per warp instruction), no smem staging, no CTA sync.
 template <int IA, int OA, bool FULL, int P, bool DIRECT = false, int NT = kNT>
 __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *sout, int tid,
-                                            int lane, uint8_t *gdst = nullptr) {
+                                            int lane, uint8_t *gdst = nullptr, bool pad = true) {
 #pragma unroll
   for (int pass = 0; pass < P; ++pass) {
     const int bo = pass * (NT * 12) + tid * 12;
@@ -260,7 +267,7 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
     }
     if (partial) {
       const int left = rem % 3;           // 1 -> "xx==", 2 -> "xxx="
-      if (left != 0) {
+      if (left != 0 && pad) {
         const int last = 4 * (rem / 3);   // first char of the partial group
         set_byte16(c, last + 3, '=');
         if (left == 1) set_byte16(c, last + 2, '=');
@@ -380,4 +387,85 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
   return errmin;
 }
 
+}  // namespace b64
+
+namespace b64 {
+// Encoded length of a tile / message of L bytes (Alg 1; NOPAD drops the '=').
+__host__ __device__ __forceinline__ int64_t enc_len(int64_t L, int flags) {
+  return (flags & kFlagNoPad) ? 4 * (L / 3) + (L % 3 ? L % 3 + 1 : 0) : 4 * ((L + 2) / 3);
+}
+
+// Final-quad / tail epilogue of one decoded stream (single buffer, shard or
+// batched message), reading R-pad / R-length and the f1/f2 variants, run by
+// one thread after every error of the stream's complete quads has been
+// reduced into err (-1 = none).  c: the stream's characters (global), m its
+// length, q4 = 4*floor(m/4); out: its output (the NOPAD tail bytes are
+// written here).  Uses the decode table g_dec_tab in shared memory.
+struct StreamResult {
+  int64_t out_len;
+  int64_t err_pos;
+  int32_t status;
+  int32_t pad_count;
+};
+
+__device__ __forceinline__ StreamResult finish_stream(const uint8_t *c, int64_t m, uint8_t *out,
+                                                      int64_t err, bool final_stream, int flags) {
+  const int64_t q = m / 4, r = m % 4;
+  StreamResult R;
+  R.pad_count = 0;
+  if (err >= 0) {
+    R.status = 1;
+    R.err_pos = err;
+    R.out_len = 3 * (err / 4);
+    return R;
+  }
+  int64_t last = -1;  // position whose trailing bits Appendix A constrains
+  uint32_t shift = 0;
+  if (r != 0) {
+    if (final_stream && (flags & kFlagNoPad) && r >= 2) {
+      uint32_t v[3] = {0, 0, 0};
+      for (int64_t i = 4 * q; i < m; ++i) {
+        const uint32_t a = g_dec_tab[c[i]];
+        if (a == kInvalid) {
+          R.status = (i == 4 * q + 2 && c[i] == '=') ? 2 : 1;
+          R.err_pos = R.status == 2 ? 4 * q : i;
+          R.out_len = 3 * q;
+          return R;
+        }
+        v[i - 4 * q] = a;
+      }
+      out[3 * q] = static_cast<uint8_t>(v[0] * 4 + v[1] / 16);
+      if (r == 3) out[3 * q + 1] = static_cast<uint8_t>((v[1] * 16) % 256 + v[2] / 4);
+      R.out_len = 3 * q + r - 1;
+      last = 4 * q + r - 1;
+      shift = r == 2 ? 16 : 64;
+    } else {
+      R.status = 2;
+      R.err_pos = 4 * q;
+      R.out_len = 3 * q;
+      return R;
+    }
+  } else {
+    int32_t p = 0;
+    if (final_stream && q > 0 && c[m - 1] == '=') p = (c[m - 2] == '=') ? 2 : 1;
+    R.pad_count = p;
+    R.out_len = 3 * q - p;
+    if (p == 2) {
+      last = m - 3;
+      shift = 16;
+    } else if (p == 1) {
+      last = m - 2;
+      shift = 64;
+    }
+  }
+  R.status = 0;
+  R.err_pos = -1;
+  if ((flags & kFlagStrict) && last >= 0 && (g_dec_tab[c[last]] * shift) % 256 != 0) {
+    R.status = 3;
+    R.err_pos = last;
+    R.out_len = 3 * (last / 4);
+    R.pad_count = 0;
+  }
+  return R;
+}
 }  // namespace b64

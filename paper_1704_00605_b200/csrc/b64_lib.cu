@@ -134,12 +134,13 @@ __device__ __forceinline__ void copy_out(uint8_t *gdst, const uint8_t *sbuf, int
 template <int IA, int OA>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     encode_kernel(const uint8_t *__restrict__ in, int64_t n, uint8_t *__restrict__ out,
-                  int64_t ntiles) {
+                  int64_t ntiles, int flags) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using G = EncS1;
   EncSmem &S = *reinterpret_cast<EncSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid));  // Table I / II
+  if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid, flags));  // Table I / II
+  const bool pad = !(flags & kFlagNoPad);
   if (tid == 0) {
     for (int s = 0; s < kStagesIn; ++s) {
       mbar_init(&S.full[s], 1);
@@ -173,52 +174,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if (d.len == G::kIn)
       encode_tile<IA, OA, true, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, tid, lane);
     else
-      encode_tile<IA, OA, false, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, tid, lane);
+      encode_tile<IA, OA, false, G::kPasses>(S.in[s] + imis, d.len, S.out[so] + omis, tid, lane,
+                                             nullptr, pad);
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[s]);
     fence_proxy_async_smem();
     if (tid == 0) bulk_wait_read<kStagesOut - 2>();  // staging slot of tile it+1 is free
     named_bar_sync(1, kNT);
-    const int olen = 4 * ((d.len + 2) / 3);
+    const int olen = static_cast<int>(enc_len(d.len, flags));
     copy_out(gdst, S.out[so] + omis, olen, tid, pol_out);
   }
   if (tid == 0) bulk_wait<0>();
 }
 
 // ------------------------------------------------------ decode kernel ---
-// Final result of a whole-stream decode (single buffer / shard).
-__device__ void finalize_single(const uint8_t *in, int64_t m, bool final_shard,
-                                unsigned long long errkey, b64_result *res) {
-  const int64_t q = m / 4, r = m % 4;
-  int32_t p = 0;
-  if (final_shard && r == 0 && q > 0 && in[m - 1] == '=') p = (in[m - 2] == '=') ? 2 : 1;
-  int64_t err = errkey == ~0ull ? -1 : static_cast<int64_t>(errkey);
-  int32_t st;
-  int64_t olen;
-  if (err < 0 && r != 0) err = 4 * q;
-  if (err < 0) {
-    st = B64_OK;
-    olen = 3 * q - p;
-  } else if (r != 0 && err == 4 * q) {
-    st = B64_ERR_LENGTH;
-    olen = 3 * q;
-    p = 0;
-  } else {
-    st = B64_ERR_INVALID_CHAR;
-    olen = 3 * (err / 4);
-    p = 0;
-  }
-  res->out_len = olen;
-  res->err_pos = err;
-  res->status = st;
-  res->pad_count = p;
-}
-
 // Single buffer / shard (rows a6-a12).
 template <int IA, int OA>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
-                  int64_t ntiles, int final_shard, DecWs *ws, b64_result *res) {
+                  int64_t ntiles, int final_shard, DecWs *ws, b64_result *res, int flags) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using G = DecS1;
   DecSmem &S = *reinterpret_cast<DecSmem *>(smem_raw);
@@ -236,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid < 64) g_dec_tab[ascii_of(tid)] = static_cast<uint8_t>(tid);
+  if (tid < 64) g_dec_tab[ascii_of(tid, flags)] = static_cast<uint8_t>(tid);
   __syncthreads();
 
   if (warp == kWarpsC) {
@@ -301,7 +275,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if (prev == gridDim.x - 1) {
       __threadfence();
       const unsigned long long e = atomicOr(&ws->errkey, 0ull);
-      finalize_single(in, m, final_shard != 0, e, res);
+      const StreamResult R = finish_stream(in, m, out, e == ~0ull ? -1 : static_cast<int64_t>(e),
+                                           final_shard != 0, flags);
+      res->out_len = R.out_len;
+      res->err_pos = R.err_pos;
+      res->status = R.status;
+      res->pad_count = R.pad_count;
       ws->errkey = ~0ull;
       ws->done = 0;
       __threadfence_system();
@@ -347,8 +326,8 @@ cudaError_t set_smem(K kernel, int bytes) {
 }
 
 // Kernel tables indexed by alignment class (0: 16-aligned, 1: 4-aligned, 2: unaligned).
-using EncFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t);
-using DecFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int, DecWs *, b64_result *);
+using EncFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int);
+using DecFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int, DecWs *, b64_result *, int);
 
 EncFn enc_table[3][3] = {
     {encode_kernel<16, 16>, encode_kernel<16, 4>, encode_kernel<16, 1>},
@@ -438,7 +417,7 @@ int64_t grid_for(int64_t ntiles, int sms) {
 }
 
 int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
-                  b64_result *d_result, cudaStream_t stream, DecWs *ws) {
+                  b64_result *d_result, cudaStream_t stream, DecWs *ws, int flags = 0) {
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   const int64_t chars = 4 * (m / 4);
@@ -446,7 +425,8 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
   const int64_t grid = grid_for(ntiles, sms);
   DecFn f = dec_table[align_class(d_in)][align_class(d_out)];
   f<<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem), stream>>>(d_in, m, d_out, ntiles,
-                                                                        final_shard, ws, d_result);
+                                                                        final_shard, ws, d_result,
+                                                                        flags);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
@@ -474,45 +454,75 @@ int64_t b64_encoded_len(int64_t n) { return n < 0 ? -1 : 4 * ((n + 2) / 3); }
 
 int64_t b64_decoded_max_len(int64_t m) { return m < 0 ? -1 : 3 * (m / 4); }
 
-int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t stream) {
-  if (n < 0 || (n > 0 && (d_in == nullptr || d_out == nullptr))) return B64_ERR_ARG;
+static bool flags_ok(int flags) { return (flags & ~(kFlagUrl | kFlagNoPad | kFlagStrict)) == 0; }
+
+int64_t b64_encoded_len_ex(int64_t n, int flags) {
+  return n < 0 || !flags_ok(flags) ? -1 : enc_len(n, flags);
+}
+
+int64_t b64_decoded_max_len_ex(int64_t m, int flags) {
+  if (m < 0 || !flags_ok(flags)) return -1;
+  const int64_t r = m % 4;
+  return 3 * (m / 4) + (((flags & kFlagNoPad) && r >= 2) ? r - 1 : 0);
+}
+
+int64_t b64_encode_ex(const uint8_t *d_in, int64_t n, uint8_t *d_out, int flags,
+                      b64_stream_t stream) {
+  if (n < 0 || !flags_ok(flags) || (n > 0 && (d_in == nullptr || d_out == nullptr)))
+    return B64_ERR_ARG;
   if (n == 0) return 0;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   const int64_t ntiles = (n + EncS1::kIn - 1) / EncS1::kIn;
   const int64_t grid = grid_for(ntiles, sms);
   EncFn f = enc_table[align_class(d_in)][align_class(d_out)];
-  f<<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem), stream>>>(d_in, n, d_out, ntiles);
+  f<<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem), stream>>>(d_in, n, d_out, ntiles,
+                                                                          flags);
   if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
-  return 4 * ((n + 2) / 3);
+  return enc_len(n, flags);
 }
 
-int b64_decode_shard_async(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
-                           b64_result *d_result, b64_stream_t stream) {
-  if (m < 0 || d_result == nullptr || (m >= 4 && (d_in == nullptr || d_out == nullptr)) ||
-      (m > 0 && d_in == nullptr))
+int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t stream) {
+  return b64_encode_ex(d_in, n, d_out, 0, stream);
+}
+
+static int decode_shard_ex(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
+                           int flags, b64_result *d_result, cudaStream_t stream) {
+  if (m < 0 || !flags_ok(flags) || d_result == nullptr ||
+      (m >= 2 && (d_in == nullptr || d_out == nullptr)) || (m > 0 && d_in == nullptr))
     return B64_ERR_ARG;
   if (!final_shard && (m % 4) != 0) return B64_ERR_ARG;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
   if (w == nullptr) return B64_ERR_CUDA;
-  return decode_launch(d_in, m, final_shard, d_out, d_result, stream, w->d_ws);
+  return decode_launch(d_in, m, final_shard, d_out, d_result, stream, w->d_ws, flags);
+}
+
+int b64_decode_shard_async(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
+                           b64_result *d_result, b64_stream_t stream) {
+  return decode_shard_ex(d_in, m, final_shard, d_out, 0, d_result, stream);
 }
 
 int b64_decode_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, b64_result *d_result,
                      b64_stream_t stream) {
-  return b64_decode_shard_async(d_in, m, 1, d_out, d_result, stream);
+  return decode_shard_ex(d_in, m, 1, d_out, 0, d_result, stream);
 }
 
-int b64_decode(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *out_len,
-               int64_t *err_pos, b64_stream_t stream) {
-  if (m < 0 || (m > 0 && d_in == nullptr) || (m >= 4 && d_out == nullptr)) return B64_ERR_ARG;
+int b64_decode_ex_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
+                        b64_result *d_result, b64_stream_t stream) {
+  return decode_shard_ex(d_in, m, 1, d_out, flags, d_result, stream);
+}
+
+int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int64_t *out_len,
+                  int64_t *err_pos, b64_stream_t stream) {
+  if (m < 0 || !flags_ok(flags) || (m > 0 && d_in == nullptr) || (m >= 2 && d_out == nullptr))
+    return B64_ERR_ARG;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
   if (w == nullptr) return B64_ERR_CUDA;
-  const int rc = decode_launch(d_in, m, 1, d_out, w->d_res, stream, w->d_ws);
+  const int rc = decode_launch(d_in, m, 1, d_out, w->d_res, stream, w->d_ws, flags);
   if (rc != B64_OK) return rc;
   if (cudaStreamSynchronize(stream) != cudaSuccess) return B64_ERR_CUDA;
   b64_result r;
@@ -520,6 +530,11 @@ int b64_decode(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *out_len,
   if (out_len) *out_len = r.out_len;
   if (err_pos) *err_pos = r.err_pos;
   return r.status;
+}
+
+int b64_decode(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *out_len,
+               int64_t *err_pos, b64_stream_t stream) {
+  return b64_decode_ex(d_in, m, d_out, 0, out_len, err_pos, stream);
 }
 
 size_t b64_batch_workspace_bytes(int64_t k, int64_t total_in, int direction) {
@@ -532,7 +547,8 @@ size_t b64_batch_workspace_bytes(int64_t k, int64_t total_in, int direction) {
 static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
                         uint8_t *d_out, int64_t *d_out_off, int64_t *d_out_len,
                         int64_t *d_err_pos, int32_t *d_status, void *d_ws, size_t ws_bytes,
-                        cudaStream_t stream, int direction) {
+                        cudaStream_t stream, int direction, int flags) {
+  if (!flags_ok(flags)) return B64_ERR_ARG;
   if (k < 0 || total_in < 0 || d_in_off == nullptr || d_out_off == nullptr || d_ws == nullptr)
     return B64_ERR_ARG;
   if (direction && k > 0 && (d_out_len == nullptr || d_err_pos == nullptr || d_status == nullptr))
@@ -565,8 +581,9 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
   int64_t *a_err = d_err_pos, *a_len = d_out_len;
   int32_t *a_st = d_status;
   unsigned int *a_done = done;
+  int a_flags = flags;
   void *args[] = {&a_in, &a_out, &a_k, &a_in_off, &a_out_off, &a_unit, &a_blk,
-                  &a_err, &a_len, &a_st, &a_done};
+                  &a_err, &a_len, &a_st, &a_done, &a_flags};
   cudaError_t e;
   if (direction) {
     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(batch_kernel<true>), dim3(grid),
@@ -579,18 +596,33 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
+int b64_encode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                        uint8_t *d_out, int64_t *d_out_off, int flags, void *d_ws, size_t ws_bytes,
+                        b64_stream_t stream) {
+  return batch_common(d_in, d_in_off, k, total_in, d_out, d_out_off, nullptr, nullptr, nullptr,
+                      d_ws, ws_bytes, stream, 0, flags);
+}
+
 int b64_encode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
                      uint8_t *d_out, int64_t *d_out_off, void *d_ws, size_t ws_bytes,
                      b64_stream_t stream) {
-  return batch_common(d_in, d_in_off, k, total_in, d_out, d_out_off, nullptr, nullptr, nullptr,
-                      d_ws, ws_bytes, stream, 0);
+  return b64_encode_batch_ex(d_in, d_in_off, k, total_in, d_out, d_out_off, 0, d_ws, ws_bytes,
+                             stream);
+}
+
+int b64_decode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
+                        uint8_t *d_out, int64_t *d_out_off, int64_t *d_out_len, int64_t *d_err_pos,
+                        int32_t *d_status, int flags, void *d_ws, size_t ws_bytes,
+                        b64_stream_t stream) {
+  return batch_common(d_in, d_in_off, k, total_in, d_out, d_out_off, d_out_len, d_err_pos,
+                      d_status, d_ws, ws_bytes, stream, 1, flags);
 }
 
 int b64_decode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
                      uint8_t *d_out, int64_t *d_out_off, int64_t *d_out_len, int64_t *d_err_pos,
                      int32_t *d_status, void *d_ws, size_t ws_bytes, b64_stream_t stream) {
-  return batch_common(d_in, d_in_off, k, total_in, d_out, d_out_off, d_out_len, d_err_pos,
-                      d_status, d_ws, ws_bytes, stream, 1);
+  return b64_decode_batch_ex(d_in, d_in_off, k, total_in, d_out, d_out_off, d_out_len, d_err_pos,
+                             d_status, 0, d_ws, ws_bytes, stream);
 }
 
 // Host-buffer entry points: the input is split into chunks; chunk i is
@@ -705,6 +737,7 @@ const char *b64_status_str(int status) {
     case B64_OK: return "ok";
     case B64_ERR_INVALID_CHAR: return "invalid character";
     case B64_ERR_LENGTH: return "length not a multiple of 4";
+    case B64_ERR_NONCANONICAL: return "non-canonical trailing bits (strict mode)";
     case B64_ERR_ARG: return "invalid argument";
     case B64_ERR_CUDA: return "CUDA error";
     case B64_ERR_WORKSPACE: return "workspace too small";
