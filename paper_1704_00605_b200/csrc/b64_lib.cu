@@ -488,8 +488,8 @@ int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t 
 
 static int decode_shard_ex(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
                            int flags, b64_result *d_result, cudaStream_t stream) {
-  if (m < 0 || !flags_ok(flags) || d_result == nullptr ||
-      (m >= 2 && (d_in == nullptr || d_out == nullptr)) || (m > 0 && d_in == nullptr))
+  if (m < 0 || !flags_ok(flags) || d_result == nullptr || (m > 0 && d_in == nullptr) ||
+      (b64_decoded_max_len_ex(m, flags) > 0 && d_out == nullptr))
     return B64_ERR_ARG;
   if (!final_shard && (m % 4) != 0) return B64_ERR_ARG;
   int dev, sms;
@@ -516,7 +516,8 @@ int b64_decode_ex_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
 
 int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int64_t *out_len,
                   int64_t *err_pos, b64_stream_t stream) {
-  if (m < 0 || !flags_ok(flags) || (m > 0 && d_in == nullptr) || (m >= 2 && d_out == nullptr))
+  if (m < 0 || !flags_ok(flags) || (m > 0 && d_in == nullptr) ||
+      (b64_decoded_max_len_ex(m, flags) > 0 && d_out == nullptr))
     return B64_ERR_ARG;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
