@@ -71,6 +71,8 @@ def _load():
                                              ctypes.POINTER(ctypes.c_int64),
                                              ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
             lib.oracle_decode_ex.restype = ctypes.c_int
+            lib.oracle_despace.argtypes = [u8p, ctypes.c_int64, u8p]
+            lib.oracle_despace.restype = ctypes.c_int64
             _lib = lib
     return _lib
 
@@ -179,3 +181,11 @@ def decode_ex(c, flags: int):
     st = lib.oracle_decode_ex(a.ctypes.data if a.size else None, a.size, out.ctypes.data,
                               ctypes.byref(ol), ctypes.byref(ep), flags)
     return int(st), int(ep.value), out[: ol.value].copy()
+
+
+def despace(a) -> np.ndarray:
+    """Appendix B scalar whitespace removal (Fig. spaceremove)."""
+    x = _as_u8(a)
+    out = np.empty(max(x.size, 1), dtype=np.uint8)
+    n = _load().oracle_despace(x.ctypes.data if x.size else None, x.size, out.ctypes.data)
+    return out[:n].copy()

@@ -295,3 +295,28 @@ int oracle_decode_ex(const uint8_t *c, int64_t m, uint8_t *p, int64_t *out_len, 
   }
   return ORACLE_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * Appendix B whitespace removal, the scalar filter
+ * of Fig. "spaceremove": copy each byte and advance the write
+ * position only when table[v] (the 256-entry keep flags) is 1.  The removed
+ * bytes are space, line feed and carriage return (the hex codes
+ * printed there are swapped, reading G8: ' ' = 0x20, '\n' = 0x0A,
+ * '\r' = 0x0D).  Out of place here (p[] separate from A[]).  Returns the new
+ * length.
+ * ------------------------------------------------------------------------ */
+int64_t oracle_despace(const uint8_t *A, int64_t N, uint8_t *p_out) {
+  uint8_t table[256];
+  int64_t i, p;
+  int v;
+  for (v = 0; v < 256; ++v) table[v] = 1;
+  table[' '] = 0;
+  table['\n'] = 0;
+  table['\r'] = 0;
+  for (i = 0, p = 0; i < N; i++) {
+    uint8_t c = A[i];
+    p_out[p] = c;
+    p += table[c];
+  }
+  return p;
+}
