@@ -33,6 +33,7 @@ EXPORTS = (
     "b64_shard", "b64_status_str", "b64_build_info",
     "b64_encoded_len_ex", "b64_decoded_max_len_ex", "b64_encode_ex", "b64_decode_ex",
     "b64_decode_ex_async", "b64_encode_batch_ex", "b64_decode_batch_ex",
+    "b64_despace_workspace_bytes", "b64_despace",
 )
 
 _lib = None
@@ -85,6 +86,8 @@ def load_library():
         "b64_decode_ex_async": (i32, [vp, i64, vp, i32, vp, vp]),
         "b64_encode_batch_ex": (i32, [vp, vp, i64, i64, vp, vp, i32, vp, sz, vp]),
         "b64_decode_batch_ex": (i32, [vp, vp, i64, i64, vp, vp, vp, vp, vp, i32, vp, sz, vp]),
+        "b64_despace_workspace_bytes": (sz, [i64]),
+        "b64_despace": (i32, [vp, i64, vp, vp, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -344,3 +347,26 @@ def b64_shard(total: int, unit: int, world: int, rank: int) -> tuple[int, int]:
     if rc < 0:
         raise B64Error(rc, "b64_shard")
     return b.value, e.value
+
+
+# ---------------------------------------------------------- whitespace ---
+
+def b64_despace(inp, out=None, ws=None, stream=None):
+    """Remove ' ', '\\n', '\\r' (Appendix B).  Returns (out, out_len_tensor);
+    the length stays on the device (int64[1]) until the caller reads it."""
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    lib = load_library()
+    m = inp.numel()
+    if out is None:
+        out = torch.empty(max(m, 1), dtype=torch.uint8, device=inp.device)
+    need = lib.b64_despace_workspace_bytes(m)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=inp.device)
+    olen = torch.empty(1, dtype=torch.int64, device=inp.device)
+    rc = lib.b64_despace(_ptr(inp), m, _ptr(out), olen.data_ptr(), ws.data_ptr(), ws.numel(),
+                         _stream(stream, inp.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_despace")
+    return out, olen

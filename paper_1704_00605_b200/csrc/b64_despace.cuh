@@ -1,0 +1,137 @@
+// b64_despace.cuh -- Appendix B whitespace removal on the GPU (SURVEY.md §8(f)
+// row f3): remove ' ' (0x20), '\n' (0x0A) and '\r' (0x0D) from a byte stream
+// (hex codes per reading G8) as a single-pass stream compaction.
+//
+// The paper's SSE kernel compacts 16 bytes with a 65,536-entry shuffle table
+// (P:1250-1271); on the GPU a warp compacts 32 bytes per step with one ballot:
+// every lane holds one byte, the kept bytes' output slots are the popcounts of
+// the ballot below each lane, so the 32 writes of a step hit consecutive smem
+// bytes (conflict-free) and input order is preserved.  A CTA takes 16 KiB
+// tiles (dynamic tile counter, TMA bulk load), each warp compacts its 1 KiB
+// segment into its own smem run, a block scan of the 16 run lengths plus a
+// decoupled look-back over the preceding tiles' totals gives every run its
+// global output offset, and the runs are written with realigned 16-byte
+// stores.  One read and one write of the data; no second pass.
+#pragma once
+#include <cstdint>
+
+#include "b64_batch.cuh"
+#include "b64_codec.cuh"
+#include "b64_ptx.cuh"
+
+namespace b64 {
+
+constexpr int kDsWarps = 16;
+constexpr int kDsThreads = kDsWarps * 32;
+constexpr int kDsSeg = 1024;                    // bytes per warp per tile
+constexpr int kDsTile = kDsWarps * kDsSeg;      // 16 KiB
+constexpr uint64_t kDsFlagAgg = 1ull << 62;     // tile aggregate published
+constexpr uint64_t kDsFlagPre = 2ull << 62;     // inclusive prefix published
+constexpr uint64_t kDsValMask = (1ull << 62) - 1;
+
+struct alignas(128) DsSmem {
+  uint8_t in[kDsTile + 32];
+  uint8_t run[kDsWarps][kDsSeg + 48];  // per-warp compacted run (16 B head room + read slack)
+  uint64_t full;
+  int64_t tile;
+  int64_t excl;
+  int32_t cnt[kDsWarps];
+  int32_t wexcl[kDsWarps];
+};
+
+__device__ __forceinline__ bool is_space(uint32_t v) {
+  return v == 0x20u || v == 0x0Au || v == 0x0Du;
+}
+
+__global__ void __launch_bounds__(kDsThreads, 1)
+    despace_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
+                   unsigned long long *state, unsigned long long *tile_ctr, int64_t *out_len,
+                   int64_t ntiles) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  DsSmem &S = *reinterpret_cast<DsSmem *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  if (tid == 0) {
+    mbar_init(&S.full, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  uint32_t phase = 0;
+  for (;;) {
+    if (tid == 0) S.tile = static_cast<int64_t>(atomicAdd(tile_ctr, 1ull));
+    __syncthreads();
+    const int64_t t = S.tile;
+    if (t >= ntiles) break;
+    const int64_t src = t * kDsTile;
+    const int L = static_cast<int>(m - src < kDsTile ? m - src : kDsTile);
+    const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src);
+    const int imis = static_cast<int>(g & 15);
+    if (tid == 0) {
+      const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
+      const uintptr_t g1 = (g + static_cast<uintptr_t>(L) + 15) & ~static_cast<uintptr_t>(15);
+      mbar_arrive_expect_tx(&S.full, static_cast<uint32_t>(g1 - g0));
+      bulk_g2s(S.in, reinterpret_cast<const void *>(g0), static_cast<uint32_t>(g1 - g0), &S.full,
+               pol);
+    }
+    mbar_wait_spin(&S.full, phase);
+    phase ^= 1;
+
+    // ---- compact this warp's segment into its run (32 bytes per ballot)
+    const uint8_t *seg = S.in + imis + warp * kDsSeg;
+    uint8_t *run = S.run[warp] + 16;
+    const int seg_len = L - warp * kDsSeg;  // may be <= 0 or > kDsSeg
+    int base = 0;
+#pragma unroll 4
+    for (int r = 0; r < kDsSeg; r += 32) {
+      const int i = r + lane;
+      const uint32_t v = seg[i];
+      const bool keep = i < seg_len && !is_space(v);
+      const unsigned b = __ballot_sync(0xffffffffu, keep);
+      if (keep) run[base + __popc(b & lt)] = static_cast<uint8_t>(v);
+      base += __popc(b);
+    }
+    if (lane == 0) S.cnt[warp] = base;
+    __syncthreads();
+
+    // ---- block scan of the run lengths + decoupled look-back over tiles
+    if (warp == 0) {
+      const int c = lane < kDsWarps ? S.cnt[lane] : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      if (lane < kDsWarps) S.wexcl[lane] = incl - c;
+      const uint64_t agg = static_cast<uint64_t>(__shfl_sync(0xffffffffu, incl, 31));
+      if (lane == 0) {
+        uint64_t excl = 0;
+        if (t == 0) {
+          atomicExch(state + 0, kDsFlagPre | agg);
+        } else {
+          atomicExch(state + t, kDsFlagAgg | agg);
+          for (int64_t j = t - 1; j >= 0; --j) {
+            uint64_t s;
+            do {
+              s = *reinterpret_cast<volatile unsigned long long *>(state + j);
+            } while ((s >> 62) == 0);
+            excl += s & kDsValMask;
+            if ((s >> 62) == 2) break;
+          }
+          atomicExch(state + t, kDsFlagPre | (excl + agg));
+        }
+        S.excl = static_cast<int64_t>(excl);
+        if (t == ntiles - 1) *out_len = static_cast<int64_t>(excl + agg);
+      }
+    }
+    __syncthreads();
+
+    // ---- write this warp's run at its global offset (realigned 16-byte stores)
+    warp_copy_out(out + S.excl + S.wexcl[warp], run, S.cnt[warp], lane);
+    fence_proxy_async_smem();  // generic reads of S.in before the next bulk write
+    __syncthreads();           // smem reused by the next tile
+  }
+}
+
+}  // namespace b64

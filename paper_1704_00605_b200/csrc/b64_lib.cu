@@ -22,6 +22,7 @@
 #include "b64_codec.cuh"
 #include "b64_ptx.cuh"
 #include "b64_batch.cuh"
+#include "b64_despace.cuh"
 
 namespace b64 {
 
@@ -363,6 +364,7 @@ bool device_setup(int *dev_out, int *sms_out) {
       for (auto f : row)
         if (set_smem(f, sizeof(DecSmem)) != cudaSuccess) return false;
     if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return false;
+    if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return false;
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return false;
     di.attrs_set = true;
   }
@@ -718,6 +720,33 @@ int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out
   if (out_len) *out_len = total;
   if (err_pos) *err_pos = -1;
   return B64_OK;
+}
+
+size_t b64_despace_workspace_bytes(int64_t m) {
+  if (m < 0) return 0;
+  const int64_t ntiles = (m + kDsTile - 1) / kDsTile;
+  return static_cast<size_t>(((ntiles + 1) * 8 + 255) / 256 * 256);
+}
+
+int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_len, void *d_ws,
+                size_t ws_bytes, b64_stream_t stream) {
+  if (m < 0 || d_out_len == nullptr || (m > 0 && (d_in == nullptr || d_out == nullptr)))
+    return B64_ERR_ARG;
+  const size_t need = b64_despace_workspace_bytes(m);
+  if (m > 0 && (d_ws == nullptr || ws_bytes < need)) return B64_ERR_WORKSPACE;
+  if (m == 0)
+    return cudaMemsetAsync(d_out_len, 0, sizeof(int64_t), stream) == cudaSuccess ? B64_OK
+                                                                                 : B64_ERR_CUDA;
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  const int64_t ntiles = (m + kDsTile - 1) / kDsTile;
+  unsigned long long *state = static_cast<unsigned long long *>(d_ws);
+  unsigned long long *ctr = state + ntiles;
+  if (cudaMemsetAsync(d_ws, 0, (ntiles + 1) * 8, stream) != cudaSuccess) return B64_ERR_CUDA;
+  const int64_t grid = ntiles < sms ? ntiles : sms;
+  despace_kernel<<<static_cast<unsigned>(grid), kDsThreads, sizeof(DsSmem), stream>>>(
+      d_in, m, d_out, state, ctr, d_out_len, ntiles);
+  return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
 int b64_shard(int64_t total, int unit, int world, int rank, int64_t *begin, int64_t *end) {
