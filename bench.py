@@ -457,6 +457,39 @@ def run_small_configs(args):
         dom, dom_ms = ("encode", enc_ms) if enc_ms >= dec_ms else ("decode", dec_ms)
         desc = "C2: 10,000 messages, log-uniform 100 B - 64 KiB (seed 1): batched encode + batched decode (incl. planner)"
         launches = 4
+    elif wl == "despace":
+        # f3: 1 GiB of MIME-style text (76-char lines + CRLF, 2.6 % whitespace),
+        # built on the device from C3-seeded bytes with our encoder + a view.
+        nraw = 57 * (1 << 24)
+        raw = torch.empty(nraw, dtype=torch.uint8, device=dev)
+        fill(raw, W.C3_SEED)
+        t = torch.empty(b64.b64_encoded_len(nraw), dtype=torch.uint8, device=dev)
+        b64.b64_encode(raw, out=t)
+        lines = t.view(-1, 76)
+        w = torch.empty(lines.shape[0], 78, dtype=torch.uint8, device=dev)
+        w[:, :76] = lines
+        w[:, 76] = 13
+        w[:, 77] = 10
+        w = w.view(-1)
+        m = w.numel()
+        out = torch.empty(m, dtype=torch.uint8, device=dev)
+        ws = torch.empty(b64.load_library().b64_despace_workspace_bytes(m), dtype=torch.uint8, device=dev)
+        olen_t = [None]
+
+        def ds():
+            olen_t[0] = b64.b64_despace(w, out=out, ws=ws)[1]
+
+        ds_ms = timed(ds)
+        kept = int(olen_t[0].item())
+        assert kept == t.numel() and torch.equal(out[:kept], t)
+        ms = ds_ms
+        value = m / (ms / 1e3) / 1e9
+        algo = {"despace": m + kept}
+        detail = {"despace_ms": ds_ms, "in_bytes": m, "out_bytes": kept,
+                  "despace_GBps_input": m / (ds_ms / 1e3) / 1e9}
+        dom, dom_ms = "despace", ds_ms
+        desc = "f3: whitespace removal of 1.27 GB MIME-style text (76-char lines + CRLF)"
+        launches = 1
     else:  # c4
         raw = torch.empty(W.C4_RAW, dtype=torch.uint8, device=dev)
         fill(raw, W.C4_SEED)
@@ -535,7 +568,7 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c5", "c3", "c1", "c2", "c4"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c3", "c1", "c2", "c4", "despace"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-bytes", type=int, default=3 << 28)
@@ -547,7 +580,7 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload in ("c1", "c2", "c4"):
+    elif args.workload in ("c1", "c2", "c4", "despace"):
         run_small_configs(args)
     else:
         run_ours(args)
