@@ -29,10 +29,12 @@ constexpr uint64_t kDsFlagAgg = 1ull << 62;     // tile aggregate published
 constexpr uint64_t kDsFlagPre = 2ull << 62;     // inclusive prefix published
 constexpr uint64_t kDsValMask = (1ull << 62) - 1;
 
+constexpr int kDsCtasPerSm = 4;
+
 struct alignas(128) DsSmem {
-  uint8_t in[kDsTile + 32];
+  uint8_t in[2][kDsTile + 32];         // double-buffered TMA input
   uint8_t run[kDsWarps][kDsSeg + 48];  // per-warp compacted run (16 B head room + read slack)
-  uint64_t full;
+  uint64_t full[2];
   int64_t tile;
   int64_t excl;
   int32_t cnt[kDsWarps];
@@ -43,7 +45,7 @@ __device__ __forceinline__ bool is_space(uint32_t v) {
   return v == 0x20u || v == 0x0Au || v == 0x0Du;
 }
 
-__global__ void __launch_bounds__(kDsThreads, 1)
+__global__ void __launch_bounds__(kDsThreads, kDsCtasPerSm)
     despace_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
                    unsigned long long *state, unsigned long long *tile_ctr, int64_t *out_len,
                    int64_t ntiles) {
@@ -52,33 +54,47 @@ __global__ void __launch_bounds__(kDsThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned lt = (1u << lane) - 1u;
   if (tid == 0) {
-    mbar_init(&S.full, 1);
+    mbar_init(&S.full[0], 1);
+    mbar_init(&S.full[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
   const uint64_t pol = policy_evict_first();
-  uint32_t phase = 0;
-  for (;;) {
-    if (tid == 0) S.tile = static_cast<int64_t>(atomicAdd(tile_ctr, 1ull));
-    __syncthreads();
-    const int64_t t = S.tile;
-    if (t >= ntiles) break;
-    const int64_t src = t * kDsTile;
+  // Issue the bulk load of tile tt into buffer b (thread 0).
+  auto load = [&](int64_t tt, int b) {
+    const int64_t src = tt * kDsTile;
     const int L = static_cast<int>(m - src < kDsTile ? m - src : kDsTile);
     const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src);
-    const int imis = static_cast<int>(g & 15);
+    const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
+    const uintptr_t g1 = (g + static_cast<uintptr_t>(L) + 15) & ~static_cast<uintptr_t>(15);
+    mbar_arrive_expect_tx(&S.full[b], static_cast<uint32_t>(g1 - g0));
+    bulk_g2s(S.in[b], reinterpret_cast<const void *>(g0), static_cast<uint32_t>(g1 - g0),
+             &S.full[b], pol);
+  };
+  // Tiles are taken from a global counter (so every tile's predecessors are
+  // already owned by running CTAs: the look-back always makes progress); the
+  // next tile is claimed and prefetched while the current one is processed.
+  if (tid == 0) {
+    S.tile = static_cast<int64_t>(atomicAdd(tile_ctr, 1ull));
+    if (S.tile < ntiles) load(S.tile, 0);
+  }
+  __syncthreads();
+  int64_t t = S.tile;
+  for (int it = 0; t < ntiles; ++it) {
+    const int b = it & 1;
+    __syncthreads();  // everyone has read S.tile (the claim of tile t)
     if (tid == 0) {
-      const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
-      const uintptr_t g1 = (g + static_cast<uintptr_t>(L) + 15) & ~static_cast<uintptr_t>(15);
-      mbar_arrive_expect_tx(&S.full, static_cast<uint32_t>(g1 - g0));
-      bulk_g2s(S.in, reinterpret_cast<const void *>(g0), static_cast<uint32_t>(g1 - g0), &S.full,
-               pol);
+      const int64_t tn = static_cast<int64_t>(atomicAdd(tile_ctr, 1ull));
+      S.tile = tn;
+      if (tn < ntiles) load(tn, b ^ 1);
     }
-    mbar_wait_spin(&S.full, phase);
-    phase ^= 1;
+    const int64_t src = t * kDsTile;
+    const int L = static_cast<int>(m - src < kDsTile ? m - src : kDsTile);
+    const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src)) & 15);
+    mbar_wait_spin(&S.full[b], static_cast<uint32_t>((it >> 1) & 1));  // buffer b's use count
 
     // ---- compact this warp's segment into its run (32 bytes per ballot)
-    const uint8_t *seg = S.in + imis + warp * kDsSeg;
+    const uint8_t *seg = S.in[b] + imis + warp * kDsSeg;
     uint8_t *run = S.run[warp] + 16;
     const int seg_len = L - warp * kDsSeg;  // may be <= 0 or > kDsSeg
     int base = 0;
@@ -129,8 +145,9 @@ __global__ void __launch_bounds__(kDsThreads, 1)
 
     // ---- write this warp's run at its global offset (realigned 16-byte stores)
     warp_copy_out(out + S.excl + S.wexcl[warp], run, S.cnt[warp], lane);
-    fence_proxy_async_smem();  // generic reads of S.in before the next bulk write
-    __syncthreads();           // smem reused by the next tile
+    fence_proxy_async_smem();  // generic reads of S.in[b] before its next bulk write
+    __syncthreads();           // runs / S.in[b] reused by the next tiles
+    t = S.tile;
   }
 }
 

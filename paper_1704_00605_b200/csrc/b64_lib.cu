@@ -743,7 +743,7 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
   unsigned long long *state = static_cast<unsigned long long *>(d_ws);
   unsigned long long *ctr = state + ntiles;
   if (cudaMemsetAsync(d_ws, 0, (ntiles + 1) * 8, stream) != cudaSuccess) return B64_ERR_CUDA;
-  const int64_t grid = ntiles < sms ? ntiles : sms;
+  const int64_t grid = ntiles < int64_t(sms) * kDsCtasPerSm ? ntiles : int64_t(sms) * kDsCtasPerSm;
   despace_kernel<<<static_cast<unsigned>(grid), kDsThreads, sizeof(DsSmem), stream>>>(
       d_in, m, d_out, state, ctr, d_out_len, ntiles);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
