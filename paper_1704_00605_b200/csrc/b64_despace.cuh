@@ -121,22 +121,35 @@ __global__ void __launch_bounds__(kDsThreads, kDsCtasPerSm)
       }
       if (lane < kDsWarps) S.wexcl[lane] = incl - c;
       const uint64_t agg = static_cast<uint64_t>(__shfl_sync(0xffffffffu, incl, 31));
-      if (lane == 0) {
-        uint64_t excl = 0;
-        if (t == 0) {
-          atomicExch(state + 0, kDsFlagPre | agg);
-        } else {
-          atomicExch(state + t, kDsFlagAgg | agg);
-          for (int64_t j = t - 1; j >= 0; --j) {
-            uint64_t s;
+      // Decoupled look-back, one warp, 32 predecessors per step: publish
+      // this tile's aggregate, then walk back until the closest tile that
+      // has published an inclusive prefix.
+      uint64_t excl = 0;
+      if (t == 0) {
+        if (lane == 0) atomicExch(state + 0, kDsFlagPre | agg);
+      } else {
+        if (lane == 0) atomicExch(state + t, kDsFlagAgg | agg);
+        int64_t j = t - 1;
+        for (;;) {
+          const int64_t idx = j - lane;
+          uint64_t st = kDsFlagPre;  // before tile 0: empty prefix
+          if (idx >= 0) {
             do {
-              s = *reinterpret_cast<volatile unsigned long long *>(state + j);
-            } while ((s >> 62) == 0);
-            excl += s & kDsValMask;
-            if ((s >> 62) == 2) break;
+              st = *reinterpret_cast<volatile unsigned long long *>(state + idx);
+            } while ((st >> 62) == 0);
           }
-          atomicExch(state + t, kDsFlagPre | (excl + agg));
+          const unsigned pre = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+          const int last = pre ? __ffs(pre) - 1 : 31;  // closest prefix (or the whole window)
+          uint64_t v = lane <= last ? (st & kDsValMask) : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          excl += v;
+          if (pre) break;
+          j -= 32;
         }
+        if (lane == 0) atomicExch(state + t, kDsFlagPre | (excl + agg));
+      }
+      if (lane == 0) {
         S.excl = static_cast<int64_t>(excl);
         if (t == ntiles - 1) *out_len = static_cast<int64_t>(excl + agg);
       }
