@@ -32,7 +32,7 @@ constexpr uint64_t kDsValMask = (1ull << 62) - 1;
 constexpr int kDsCtasPerSm = 4;
 
 struct alignas(128) DsSmem {
-  uint8_t in[2][kDsTile + 32];         // double-buffered TMA input
+  uint8_t in[2][kDsTile + 48];         // double-buffered TMA input (+ funnel-load slack)
   uint8_t run[kDsWarps][kDsSeg + 48];  // per-warp compacted run (16 B head room + read slack)
   uint64_t full[2];
   int64_t tile;
@@ -52,7 +52,6 @@ __global__ void __launch_bounds__(kDsThreads, kDsCtasPerSm)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   DsSmem &S = *reinterpret_cast<DsSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const unsigned lt = (1u << lane) - 1u;
   if (tid == 0) {
     mbar_init(&S.full[0], 1);
     mbar_init(&S.full[1], 1);
@@ -93,19 +92,50 @@ __global__ void __launch_bounds__(kDsThreads, kDsCtasPerSm)
     const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src)) & 15);
     mbar_wait_spin(&S.full[b], static_cast<uint32_t>((it >> 1) & 1));  // buffer b's use count
 
-    // ---- compact this warp's segment into its run (32 bytes per ballot)
+    // ---- compact this warp's segment into its run, 128 bytes per step:
+    // each lane takes one 4-byte word; an exact SWAR test finds bytes below
+    // 0x21 (only then are the three whitespace values checked one by one);
+    // a warp scan of the per-lane kept counts places every kept byte, so
+    // the byte stores of a step hit consecutive smem words (conflict-free)
+    // and input order is preserved.
     const uint8_t *seg = S.in[b] + imis + warp * kDsSeg;
     uint8_t *run = S.run[warp] + 16;
     const int seg_len = L - warp * kDsSeg;  // may be <= 0 or > kDsSeg
+    const uint32_t sh = 8u * static_cast<uint32_t>(reinterpret_cast<uintptr_t>(seg) & 3);
+    const uint32_t *segw = reinterpret_cast<const uint32_t *>(seg - (reinterpret_cast<uintptr_t>(seg) & 3));
     int base = 0;
-#pragma unroll 4
-    for (int r = 0; r < kDsSeg; r += 32) {
-      const int i = r + lane;
-      const uint32_t v = seg[i];
-      const bool keep = i < seg_len && !is_space(v);
-      const unsigned b = __ballot_sync(0xffffffffu, keep);
-      if (keep) run[base + __popc(b & lt)] = static_cast<uint8_t>(v);
-      base += __popc(b);
+#pragma unroll 2
+    for (int r = 0; r < kDsSeg / 4; r += 32) {
+      const int wi = r + lane;  // word index in the segment
+      const uint32_t w = __funnelshift_r(segw[wi], segw[wi + 1], sh);
+      uint32_t keep = 0xFu;
+      const int valid = seg_len - 4 * wi;  // bytes of this word inside the tile
+      if (valid < 4) keep = valid <= 0 ? 0u : (1u << valid) - 1u;
+      const uint32_t low = ~((w | 0x80808080u) - 0x21212121u) & ~w & 0x80808080u;  // bytes < 0x21
+      if (low) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (is_space((w >> (8 * j)) & 0xFFu)) keep &= ~(1u << j);
+      }
+      const int c = __popc(keep);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      uint8_t *p = run + base + (incl - c);
+      if (keep == 0xFu) {
+        p[0] = static_cast<uint8_t>(w);
+        p[1] = static_cast<uint8_t>(w >> 8);
+        p[2] = static_cast<uint8_t>(w >> 16);
+        p[3] = static_cast<uint8_t>(w >> 24);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (keep & (1u << j)) *p++ = static_cast<uint8_t>(w >> (8 * j));
+      }
+      base += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) S.cnt[warp] = base;
     __syncthreads();
