@@ -183,9 +183,9 @@ int b64_decode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
 /* Appendix B: remove ' ' (0x20), '\n' (0x0A) and '\r' (0x0D)
  * from d_in[0..m) into d_out (capacity m; d_out must not overlap d_in),
  * preserving order; *d_out_len (device int64) receives the new length.
- * Single pass: ballot-based warp compaction + decoupled look-back scan over
- * 16 KiB tiles.  d_ws: b64_despace_workspace_bytes(m) bytes of device
- * memory (zeroed by the call).  Asynchronous. */
+ * Two kernels: per-chunk kept counts, then warp-scan compaction of 16 KiB
+ * tiles at the chunk offsets.  d_ws: b64_despace_workspace_bytes(m) bytes of
+ * device memory.  Asynchronous. */
 size_t b64_despace_workspace_bytes(int64_t m);
 int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_len, void *d_ws,
                 size_t ws_bytes, b64_stream_t stream);

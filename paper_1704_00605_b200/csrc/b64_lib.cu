@@ -724,28 +724,30 @@ int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out
 
 size_t b64_despace_workspace_bytes(int64_t m) {
   if (m < 0) return 0;
-  const int64_t ntiles = (m + kDsTile - 1) / kDsTile;
-  return static_cast<size_t>(((ntiles + 1) * 8 + 255) / 256 * 256);
+  return 8 * 4096;  // per-chunk kept counts (<= 4096 chunks)
 }
 
 int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_len, void *d_ws,
                 size_t ws_bytes, b64_stream_t stream) {
   if (m < 0 || d_out_len == nullptr || (m > 0 && (d_in == nullptr || d_out == nullptr)))
     return B64_ERR_ARG;
-  const size_t need = b64_despace_workspace_bytes(m);
-  if (m > 0 && (d_ws == nullptr || ws_bytes < need)) return B64_ERR_WORKSPACE;
+  if (m > 0 && (d_ws == nullptr || ws_bytes < b64_despace_workspace_bytes(m)))
+    return B64_ERR_WORKSPACE;
   if (m == 0)
     return cudaMemsetAsync(d_out_len, 0, sizeof(int64_t), stream) == cudaSuccess ? B64_OK
                                                                                  : B64_ERR_CUDA;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   const int64_t ntiles = (m + kDsTile - 1) / kDsTile;
-  unsigned long long *state = static_cast<unsigned long long *>(d_ws);
-  unsigned long long *ctr = state + ntiles;
-  if (cudaMemsetAsync(d_ws, 0, (ntiles + 1) * 8, stream) != cudaSuccess) return B64_ERR_CUDA;
-  const int64_t grid = ntiles < int64_t(sms) * kDsCtasPerSm ? ntiles : int64_t(sms) * kDsCtasPerSm;
+  int64_t ctas = static_cast<int64_t>(sms) * kDsCtasPerSm;
+  if (ctas > 4096) ctas = 4096;
+  const int64_t tpc = (ntiles + ctas - 1) / ctas;    // tiles per chunk
+  const int64_t grid = (ntiles + tpc - 1) / tpc;      // chunks
+  int64_t *counts = static_cast<int64_t *>(d_ws);
+  despace_count_kernel<<<static_cast<unsigned>(grid), kDsThreads, 0, stream>>>(d_in, m, tpc,
+                                                                                counts);
   despace_kernel<<<static_cast<unsigned>(grid), kDsThreads, sizeof(DsSmem), stream>>>(
-      d_in, m, d_out, state, ctr, d_out_len, ntiles);
+      d_in, m, d_out, counts, tpc, d_out_len, ntiles);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
