@@ -45,24 +45,29 @@ __device__ __forceinline__ bool is_space(uint32_t v) {
   return v == 0x20u || v == 0x0Au || v == 0x0Du;
 }
 
-// Kept-byte count of 16 bytes (4 words, little-endian).
-__device__ __forceinline__ int kept16(const uint4 &v, int valid) {
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    uint32_t keep = 0xFu;
-    const int vb = valid - 4 * k;
-    if (vb < 4) keep = vb <= 0 ? 0u : (1u << vb) - 1u;
-    const uint32_t low = ~((w[k] | 0x80808080u) - 0x21212121u) & ~w[k] & 0x80808080u;
-    if (low) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (is_space((w[k] >> (8 * j)) & 0xFFu)) keep &= ~(1u << j);
-    }
-    c += __popc(keep);
+// Per-byte flags (0x80 in each byte) of the bytes below 0x21 in w (exact:
+// no cross-byte borrows because every byte of (w | 0x80808080) is >= 0x80).
+__device__ __forceinline__ uint32_t below21(uint32_t w) {
+  return ~((w | 0x80808080u) - 0x21212121u) & ~w & 0x80808080u;
+}
+
+// Remove from keep (one bit per byte) the flagged bytes that are whitespace
+// (the flagged set is tiny: CR / LF in MIME text).
+__device__ __forceinline__ uint32_t drop_spaces(uint32_t w, uint32_t low, uint32_t keep) {
+  while (low) {
+    const int bit = __ffs(low) - 1;  // 7, 15, 23 or 31
+    if (is_space((w >> (bit - 7)) & 0xFFu)) keep &= ~(1u << (bit >> 3));
+    low &= low - 1;
   }
-  return c;
+  return keep;
+}
+
+// Kept-byte count of 16 bytes.
+__device__ __forceinline__ int kept16(const uint4 &v) {
+  const uint32_t l0 = below21(v.x), l1 = below21(v.y), l2 = below21(v.z), l3 = below21(v.w);
+  if ((l0 | l1 | l2 | l3) == 0) return 16;
+  return __popc(drop_spaces(v.x, l0, 0xFu)) + __popc(drop_spaces(v.y, l1, 0xFu)) +
+         __popc(drop_spaces(v.z, l2, 0xFu)) + __popc(drop_spaces(v.w, l3, 0xFu));
 }
 
 // Pass 1: kept bytes of chunk b = tiles [b*tpc, (b+1)*tpc).
@@ -80,7 +85,7 @@ __global__ void __launch_bounds__(kDsThreads)
     if (threadIdx.x < h) cnt += !is_space(in[c0 + threadIdx.x]);
     const uint4 *q = reinterpret_cast<const uint4 *>(in + c0 + h);
     const int64_t ng = (c1 - c0 - h) / 16;
-    for (int64_t i = threadIdx.x; i < ng; i += kDsThreads) cnt += kept16(__ldcs(q + i), 16);
+    for (int64_t i = threadIdx.x; i < ng; i += kDsThreads) cnt += kept16(__ldcs(q + i));
     const int64_t t0 = c0 + h + 16 * ng;
     if (threadIdx.x < c1 - t0) cnt += !is_space(in[t0 + threadIdx.x]);
   }
@@ -149,39 +154,38 @@ __global__ void __launch_bounds__(kDsThreads, kDsCtasPerSm)
     const int seg_len = L - warp * kDsSeg;  // may be <= 0 or > kDsSeg
     const uint32_t sh = 8u * static_cast<uint32_t>(reinterpret_cast<uintptr_t>(seg) & 3);
     const uint32_t *segw = reinterpret_cast<const uint32_t *>(seg - (reinterpret_cast<uintptr_t>(seg) & 3));
+    const unsigned lt = (1u << lane) - 1u;
     int base = 0;
 #pragma unroll 2
     for (int r = 0; r < kDsSeg / 4; r += 32) {
       const int wi = r + lane;  // word index in the segment
       const uint32_t w = __funnelshift_r(segw[wi], segw[wi + 1], sh);
       uint32_t keep = 0xFu;
-      const int valid = seg_len - 4 * wi;  // bytes of this word inside the tile
-      if (valid < 4) keep = valid <= 0 ? 0u : (1u << valid) - 1u;
-      const uint32_t low = ~((w | 0x80808080u) - 0x21212121u) & ~w & 0x80808080u;  // bytes < 0x21
-      if (low) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (is_space((w >> (8 * j)) & 0xFFu)) keep &= ~(1u << j);
+      if (L < kDsTile) {  // last tile only
+        const int valid = seg_len - 4 * wi;
+        if (valid < 4) keep = valid <= 0 ? 0u : (1u << valid) - 1u;
       }
-      const int c = __popc(keep);
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
-      }
-      uint8_t *p = run + base + (incl - c);
+      const uint32_t low = below21(w);
+      if (low) keep = drop_spaces(w, low, keep);
+      const uint32_t c = __popc(keep);
+      // warp exclusive scan of c (0..4) by its three bit planes
+      const unsigned b0 = __ballot_sync(0xffffffffu, c & 1u);
+      const unsigned b1 = __ballot_sync(0xffffffffu, c & 2u);
+      const unsigned b2 = __ballot_sync(0xffffffffu, c & 4u);
+      const int excl = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+      uint8_t *p = run + base + excl;
       if (keep == 0xFu) {
         p[0] = static_cast<uint8_t>(w);
         p[1] = static_cast<uint8_t>(w >> 8);
         p[2] = static_cast<uint8_t>(w >> 16);
         p[3] = static_cast<uint8_t>(w >> 24);
       } else {
+        int k = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (keep & (1u << j)) *p++ = static_cast<uint8_t>(w >> (8 * j));
+          if (keep & (1u << j)) p[k++] = static_cast<uint8_t>(w >> (8 * j));
       }
-      base += __shfl_sync(0xffffffffu, incl, 31);
+      base += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
     }
     if (lane == 0) S.cnt[warp] = base;
     __syncthreads();
