@@ -51,23 +51,21 @@ __device__ __forceinline__ uint32_t below21(uint32_t w) {
   return ~((w | 0x80808080u) - 0x21212121u) & ~w & 0x80808080u;
 }
 
-// Remove from keep (one bit per byte) the flagged bytes that are whitespace
-// (the flagged set is tiny: CR / LF in MIME text).
-__device__ __forceinline__ uint32_t drop_spaces(uint32_t w, uint32_t low, uint32_t keep) {
-  while (low) {
-    const int bit = __ffs(low) - 1;  // 7, 15, 23 or 31
-    if (is_space((w >> (bit - 7)) & 0xFFu)) keep &= ~(1u << (bit >> 3));
-    low &= low - 1;
-  }
-  return keep;
+// Exact per-byte whitespace flags (0x80 in each byte that is 0x20, 0x0A or
+// 0x0D), branch-free: among the bytes below 0x21, 0x20 is the only one with
+// bit 5 set, and x == K is tested on the low 7 bits (no carries: every byte
+// of (x & 0x7F..) + 0x7F.. is <= 0xFE); bytes >= 0x80 are excluded by below21.
+__device__ __forceinline__ uint32_t space_flags(uint32_t w) {
+  const uint32_t low = below21(w);
+  const uint32_t t1 = ((w ^ 0x0A0A0A0Au) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;  // bit 7 clear iff == 0x0A
+  const uint32_t t2 = ((w ^ 0x0D0D0D0Du) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;  // bit 7 clear iff == 0x0D
+  return low & (~(t1 & t2) | (w << 2));
 }
 
 // Kept-byte count of 16 bytes.
 __device__ __forceinline__ int kept16(const uint4 &v) {
-  const uint32_t l0 = below21(v.x), l1 = below21(v.y), l2 = below21(v.z), l3 = below21(v.w);
-  if ((l0 | l1 | l2 | l3) == 0) return 16;
-  return __popc(drop_spaces(v.x, l0, 0xFu)) + __popc(drop_spaces(v.y, l1, 0xFu)) +
-         __popc(drop_spaces(v.z, l2, 0xFu)) + __popc(drop_spaces(v.w, l3, 0xFu));
+  return 16 - __popc(space_flags(v.x)) - __popc(space_flags(v.y)) - __popc(space_flags(v.z)) -
+         __popc(space_flags(v.w));
 }
 
 // Pass 1: kept bytes of chunk b = tiles [b*tpc, (b+1)*tpc).
@@ -165,8 +163,8 @@ __global__ void __launch_bounds__(kDsThreads, kDsCtasPerSm)
         const int valid = seg_len - 4 * wi;
         if (valid < 4) keep = valid <= 0 ? 0u : (1u << valid) - 1u;
       }
-      const uint32_t low = below21(w);
-      if (low) keep = drop_spaces(w, low, keep);
+      const uint32_t sp = space_flags(w);
+      keep &= ~((sp >> 7) & 1u | (sp >> 14) & 2u | (sp >> 21) & 4u | (sp >> 28) & 8u);
       const uint32_t c = __popc(keep);
       // warp exclusive scan of c (0..4) by its three bit planes
       const unsigned b0 = __ballot_sync(0xffffffffu, c & 1u);
