@@ -83,7 +83,13 @@ __global__ void __launch_bounds__(kDsThreads)
     if (threadIdx.x < h) cnt += !is_space(in[c0 + threadIdx.x]);
     const uint4 *q = reinterpret_cast<const uint4 *>(in + c0 + h);
     const int64_t ng = (c1 - c0 - h) / 16;
-    for (int64_t i = threadIdx.x; i < ng; i += kDsThreads) cnt += kept16(__ldcs(q + i));
+    int64_t i = threadIdx.x;
+    for (; i + 3 * kDsThreads < ng; i += 4 * kDsThreads) {
+      const uint4 a = __ldcs(q + i), b = __ldcs(q + i + kDsThreads);
+      const uint4 c = __ldcs(q + i + 2 * kDsThreads), d = __ldcs(q + i + 3 * kDsThreads);
+      cnt += kept16(a) + kept16(b) + kept16(c) + kept16(d);
+    }
+    for (; i < ng; i += kDsThreads) cnt += kept16(__ldcs(q + i));
     const int64_t t0 = c0 + h + 16 * ng;
     if (threadIdx.x < c1 - t0) cnt += !is_space(in[t0 + threadIdx.x]);
   }
@@ -158,13 +164,13 @@ __global__ void __launch_bounds__(kDsThreads, kDsCtasPerSm)
     for (int r = 0; r < kDsSeg / 4; r += 32) {
       const int wi = r + lane;  // word index in the segment
       const uint32_t w = __funnelshift_r(segw[wi], segw[wi + 1], sh);
-      uint32_t keep = 0xFu;
+      // keep bits 0..3 = bytes that are not whitespace: gather bit 7 of
+      // every byte of ~flags into bits 28..31 with one multiply
+      uint32_t keep = ((~space_flags(w) & 0x80808080u) * 0x00204081u) >> 28;
       if (L < kDsTile) {  // last tile only
         const int valid = seg_len - 4 * wi;
-        if (valid < 4) keep = valid <= 0 ? 0u : (1u << valid) - 1u;
+        if (valid < 4) keep &= valid <= 0 ? 0u : (1u << valid) - 1u;
       }
-      const uint32_t sp = space_flags(w);
-      keep &= ~((sp >> 7) & 1u | (sp >> 14) & 2u | (sp >> 21) & 4u | (sp >> 28) & 8u);
       const uint32_t c = __popc(keep);
       // warp exclusive scan of c (0..4) by its three bit planes
       const unsigned b0 = __ballot_sync(0xffffffffu, c & 1u);
@@ -172,17 +178,11 @@ __global__ void __launch_bounds__(kDsThreads, kDsCtasPerSm)
       const unsigned b2 = __ballot_sync(0xffffffffu, c & 4u);
       const int excl = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
       uint8_t *p = run + base + excl;
-      if (keep == 0xFu) {
-        p[0] = static_cast<uint8_t>(w);
-        p[1] = static_cast<uint8_t>(w >> 8);
-        p[2] = static_cast<uint8_t>(w >> 16);
-        p[3] = static_cast<uint8_t>(w >> 24);
-      } else {
-        int k = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (keep & (1u << j)) p[k++] = static_cast<uint8_t>(w >> (8 * j));
-      }
+      // branch-free placement: byte j goes to p[popc(keep & ((1 << j) - 1))]
+      if (keep & 1u) p[0] = static_cast<uint8_t>(w);
+      if (keep & 2u) p[keep & 1u] = static_cast<uint8_t>(w >> 8);
+      if (keep & 4u) p[__popc(keep & 3u)] = static_cast<uint8_t>(w >> 16);
+      if (keep & 8u) p[__popc(keep & 7u)] = static_cast<uint8_t>(w >> 24);
       base += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
     }
     if (lane == 0) S.cnt[warp] = base;
