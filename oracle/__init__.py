@@ -73,6 +73,16 @@ def _load():
             lib.oracle_decode_ex.restype = ctypes.c_int
             lib.oracle_despace.argtypes = [u8p, ctypes.c_int64, u8p]
             lib.oracle_despace.restype = ctypes.c_int64
+            lib.oracle_encoded_len_wrapped.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                                       ctypes.c_int]
+            lib.oracle_encoded_len_wrapped.restype = ctypes.c_int64
+            lib.oracle_encode_wrapped.argtypes = [u8p, ctypes.c_int64, u8p, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_int]
+            lib.oracle_encode_wrapped.restype = ctypes.c_int64
+            lib.oracle_decode_ws.argtypes = [u8p, ctypes.c_int64, u8p,
+                                             ctypes.POINTER(ctypes.c_int64),
+                                             ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+            lib.oracle_decode_ws.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -189,3 +199,30 @@ def despace(a) -> np.ndarray:
     out = np.empty(max(x.size, 1), dtype=np.uint8)
     n = _load().oracle_despace(x.ctypes.data if x.size else None, x.size, out.ctypes.data)
     return out[:n].copy()
+
+
+def encode_wrapped(s, line_chars: int = 76, crlf: bool = False, flags: int = 0) -> np.ndarray:
+    """f4: Algorithm 1, then an EOL after every ``line_chars`` characters and
+    after the final line (MIME / PEM style)."""
+    a = _as_u8(s)
+    lib = _load()
+    out = np.empty(max(lib.oracle_encoded_len_wrapped(a.size, line_chars, int(crlf), flags), 1),
+                   dtype=np.uint8)
+    w = lib.oracle_encode_wrapped(a.ctypes.data if a.size else None, a.size, out.ctypes.data,
+                                  line_chars, int(crlf), flags)
+    assert w >= 0
+    return out[:w].copy()
+
+
+def decode_ws(c, flags: int = 0):
+    """f4: Appendix B whitespace filter, then Algorithm 2; err_pos in the
+    coordinates of the original input.  Returns (status, err_pos, out)."""
+    a = _as_u8(c)
+    lib = _load()
+    out = np.empty(3 * (a.size // 4) + 3, dtype=np.uint8)
+    ol = ctypes.c_int64(0)
+    ep = ctypes.c_int64(0)
+    st = lib.oracle_decode_ws(a.ctypes.data if a.size else None, a.size, out.ctypes.data,
+                              ctypes.byref(ol), ctypes.byref(ep), flags)
+    assert st >= 0
+    return int(st), int(ep.value), out[: ol.value].copy()

@@ -320,3 +320,78 @@ int64_t oracle_despace(const uint8_t *A, int64_t N, uint8_t *p_out) {
   }
   return p;
 }
+
+/* ------------------------------------------------------------------------
+ * MIME-style line handling.
+ *
+ * The paper's comparison includes a codec (Linux) that tolerates line feeds
+ * between blocks of four characters, and Appendix B says
+ * white space "should be removed prior to processing".  Two plain
+ * compositions of the functions above (reading R-ws-decode / R-wrap in
+ * DESIGN.md §3):
+ *
+ *   oracle_encode_wrapped  Algorithm 1 (with the f1 variant flags), then the
+ *                          end-of-line sequence (LF, or CR LF when crlf != 0)
+ *                          inserted after every line_chars characters and
+ *                          after the final, possibly shorter, line (no EOL
+ *                          for an empty output).  line_chars is a positive
+ *                          multiple of 4 (76 for MIME, RFC 2045; 64 for PEM).
+ *   oracle_decode_ws       the Appendix B filter (oracle_despace's table:
+ *                          ' ', '\n', '\r') applied first, then Algorithm 2
+ *                          (oracle_decode_ex, same flags) on the kept bytes;
+ *                          an error offset is reported in the coordinates of
+ *                          the ORIGINAL input: the position of the kept byte
+ *                          the decoder rejected.
+ * ------------------------------------------------------------------------ */
+#include <stdlib.h>
+
+int64_t oracle_encoded_len_wrapped(int64_t n, int line_chars, int crlf, int flags) {
+  const int64_t m = oracle_encoded_len_ex(n, flags);
+  const int64_t lines = (m + line_chars - 1) / line_chars;
+  return m + lines * (crlf ? 2 : 1);
+}
+
+int64_t oracle_encode_wrapped(const uint8_t *s, int64_t n, uint8_t *p, int line_chars, int crlf,
+                              int flags) {
+  const int64_t m = oracle_encoded_len_ex(n, flags);
+  uint8_t *t = (uint8_t *)malloc(m > 0 ? (size_t)m : 1);
+  int64_t j, o = 0;
+  if (!t) return -1;
+  oracle_encode_ex(s, n, t, flags); /* Algorithm 1 */
+  for (j = 0; j < m; ++j) {
+    p[o++] = t[j];
+    if ((j + 1) % line_chars == 0 || j == m - 1) { /* end of a line */
+      if (crlf) p[o++] = '\r';
+      p[o++] = '\n';
+    }
+  }
+  free(t);
+  return o;
+}
+
+/* p must hold 3*floor(m/4) + 2 bytes. */
+int oracle_decode_ws(const uint8_t *c, int64_t m, uint8_t *p, int64_t *out_len, int64_t *err_pos,
+                     int flags) {
+  uint8_t *t = (uint8_t *)malloc(m > 0 ? (size_t)m : 1);
+  int64_t *orig = (int64_t *)malloc(m > 0 ? (size_t)m * sizeof(int64_t) : sizeof(int64_t));
+  int64_t i, k = 0;
+  int st;
+  if (!t || !orig) {
+    free(t);
+    free(orig);
+    return -1;
+  }
+  /* Appendix B filter (Fig. spaceremove), remembering where
+   * each kept byte came from */
+  for (i = 0; i < m; ++i) {
+    if (c[i] == ' ' || c[i] == '\n' || c[i] == '\r') continue;
+    t[k] = c[i];
+    orig[k] = i;
+    ++k;
+  }
+  st = oracle_decode_ex(t, k, p, out_len, err_pos, flags); /* Algorithm 2 */
+  if (*err_pos >= 0) *err_pos = orig[*err_pos];
+  free(t);
+  free(orig);
+  return st;
+}
