@@ -489,7 +489,7 @@ def run_small_configs(args):
                   "despace_GBps_input": m / (ds_ms / 1e3) / 1e9}
         dom, dom_ms = "despace", ds_ms
         desc = "f3: whitespace removal of 1.27 GB MIME-style text (76-char lines + CRLF)"
-        launches = 1
+        launches = 2
     else:  # c4
         raw = torch.empty(W.C4_RAW, dtype=torch.uint8, device=dev)
         fill(raw, W.C4_SEED)

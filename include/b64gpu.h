@@ -183,12 +183,35 @@ int b64_decode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
 /* Appendix B: remove ' ' (0x20), '\n' (0x0A) and '\r' (0x0D)
  * from d_in[0..m) into d_out (capacity m; d_out must not overlap d_in),
  * preserving order; *d_out_len (device int64) receives the new length.
- * Two kernels: per-chunk kept counts, then warp-scan compaction of 16 KiB
- * tiles at the chunk offsets.  d_ws: b64_despace_workspace_bytes(m) bytes of
+ * Two kernels: per-chunk kept counts, then per-chunk compaction of 16 KiB
+ * TMA-staged tiles (warp scans, congruent 16-byte copy-out) at the chunk
+ * offsets.  d_ws: b64_despace_workspace_bytes(m) bytes of
  * device memory.  Asynchronous. */
 size_t b64_despace_workspace_bytes(int64_t m);
 int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_len, void *d_ws,
                 size_t ws_bytes, b64_stream_t stream);
+
+/* -------------------------------------------- MIME line handling (f4) */
+
+/* Whitespace-tolerant decode (reading R-ws-decode): the
+ * Appendix B filter ("white-space characters ... should be removed
+ * prior to processing"; removed set ' ', '\n', '\r') followed
+ * by Algorithm 2 with variant `flags` on the kept characters --
+ * fused: the compacted text never leaves shared memory.  Accepts e.g. MIME
+ * text with CRLF every 76 characters, or the Linux codec's line feeds
+ * between quads.  Every error offset (INVALID_CHAR, LENGTH,
+ * NONCANONICAL) is an offset into d_in (ORIGINAL coordinates: the position
+ * of the kept byte the decoder rejected); out_len counts decoded bytes.
+ * d_out capacity: b64_decoded_max_len_ex(m, flags).  d_ws: device scratch
+ * of b64_decode_ws_workspace_bytes(m) bytes, 16-byte aligned, not shared
+ * with a concurrent call.  Two kernels on `stream`.
+ * _async writes the result record to d_result (device memory); the plain
+ * call synchronizes `stream` and returns the status. */
+size_t b64_decode_ws_workspace_bytes(int64_t m);
+int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
+                        b64_result *d_result, void *d_ws, size_t ws_bytes, b64_stream_t stream);
+int b64_decode_ws(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int64_t *out_len,
+                  int64_t *err_pos, void *d_ws, size_t ws_bytes, b64_stream_t stream);
 
 /* ------------------------------------------------------------ host buffers */
 

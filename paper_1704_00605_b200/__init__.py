@@ -20,6 +20,9 @@ from ._lib import (  # noqa: F401
     B64_FLAG_URL,
     b64_decode_ex,
     b64_despace,
+    b64_decode_ws,
+    b64_decode_ws_async,
+    b64_decode_ws_workspace_bytes,
     b64_decode_ex_async,
     b64_decoded_max_len_ex,
     b64_encode_ex,

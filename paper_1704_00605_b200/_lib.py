@@ -34,6 +34,7 @@ EXPORTS = (
     "b64_encoded_len_ex", "b64_decoded_max_len_ex", "b64_encode_ex", "b64_decode_ex",
     "b64_decode_ex_async", "b64_encode_batch_ex", "b64_decode_batch_ex",
     "b64_despace_workspace_bytes", "b64_despace",
+    "b64_decode_ws_workspace_bytes", "b64_decode_ws", "b64_decode_ws_async",
 )
 
 _lib = None
@@ -88,6 +89,10 @@ def load_library():
         "b64_decode_batch_ex": (i32, [vp, vp, i64, i64, vp, vp, vp, vp, vp, i32, vp, sz, vp]),
         "b64_despace_workspace_bytes": (sz, [i64]),
         "b64_despace": (i32, [vp, i64, vp, vp, vp, sz, vp]),
+        "b64_decode_ws_workspace_bytes": (sz, [i64]),
+        "b64_decode_ws_async": (i32, [vp, i64, vp, i32, vp, vp, sz, vp]),
+        "b64_decode_ws": (i32, [vp, i64, vp, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), vp, sz,
+                                vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -370,3 +375,63 @@ def b64_despace(inp, out=None, ws=None, stream=None):
     if rc < 0:
         raise B64Error(rc, "b64_despace")
     return out, olen
+
+
+# ------------------------------------------------- MIME line handling ---
+
+def b64_decode_ws_workspace_bytes(m: int) -> int:
+    return load_library().b64_decode_ws_workspace_bytes(m)
+
+
+def _ws_scratch(m, device, ws):
+    import torch
+
+    need = b64_decode_ws_workspace_bytes(m)
+    if ws is None or ws.numel() < need or ws.data_ptr() % 16:
+        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=device)
+    return ws
+
+
+def b64_decode_ws(inp, out=None, flags: int = 0, ws=None, stream=None):
+    """Whitespace-tolerant decode (App. B filter + Alg 2, fused).  Returns
+    (out[:out_len], status, err_pos); err_pos is an offset into ``inp``."""
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    lib = load_library()
+    m = inp.numel()
+    cap = lib.b64_decoded_max_len_ex(m, flags)
+    if out is None:
+        out = torch.empty(max(cap, 1), dtype=torch.uint8, device=inp.device)
+    else:
+        _check_u8_cuda(out, "out")
+        if out.numel() < cap:
+            raise ValueError("out too small")
+    ws = _ws_scratch(m, inp.device, ws)
+    ol = ctypes.c_int64(0)
+    ep = ctypes.c_int64(0)
+    st = lib.b64_decode_ws(_ptr(inp), m, _ptr(out), flags, ctypes.byref(ol), ctypes.byref(ep),
+                           ws.data_ptr(), ws.numel(), _stream(stream, inp.device))
+    if st < 0:
+        raise B64Error(st, "b64_decode_ws")
+    return out[: ol.value], st, ep.value
+
+
+def b64_decode_ws_async(inp, out, result, flags: int = 0, ws=None, stream=None):
+    """Asynchronous whitespace-tolerant decode; the b64_result record lands in
+    ``result`` (int64[3] CUDA tensor, see unpack_result)."""
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    _check_u8_cuda(out, "out")
+    if not (result.is_cuda and result.dtype == torch.int64 and result.numel() >= 3):
+        raise TypeError("result must be an int64[3] CUDA tensor")
+    lib = load_library()
+    m = inp.numel()
+    if out.numel() < lib.b64_decoded_max_len_ex(m, flags):
+        raise ValueError("out too small")
+    ws = _ws_scratch(m, inp.device, ws)
+    rc = lib.b64_decode_ws_async(_ptr(inp), m, _ptr(out), flags, result.data_ptr(), ws.data_ptr(),
+                                 ws.numel(), _stream(stream, inp.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_decode_ws_async")

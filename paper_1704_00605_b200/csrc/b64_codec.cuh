@@ -408,8 +408,12 @@ struct StreamResult {
   int32_t pad_count;
 };
 
-__device__ __forceinline__ StreamResult finish_stream(const uint8_t *c, int64_t m, uint8_t *out,
-                                                      int64_t err, bool final_stream, int flags) {
+// CharAt: c(i) returns character i of the stream (only i >= 4*floor((m-1)/4),
+// i.e. the final quad, is ever read).
+template <class CharAt>
+__device__ __forceinline__ StreamResult finish_stream_at(const CharAt &c, int64_t m, uint8_t *out,
+                                                         int64_t err, bool final_stream,
+                                                         int flags) {
   const int64_t q = m / 4, r = m % 4;
   StreamResult R;
   R.pad_count = 0;
@@ -425,9 +429,9 @@ __device__ __forceinline__ StreamResult finish_stream(const uint8_t *c, int64_t 
     if (final_stream && (flags & kFlagNoPad) && r >= 2) {
       uint32_t v[3] = {0, 0, 0};
       for (int64_t i = 4 * q; i < m; ++i) {
-        const uint32_t a = g_dec_tab[c[i]];
+        const uint32_t a = g_dec_tab[c(i)];
         if (a == kInvalid) {
-          R.status = (i == 4 * q + 2 && c[i] == '=') ? 2 : 1;
+          R.status = (i == 4 * q + 2 && c(i) == '=') ? 2 : 1;
           R.err_pos = R.status == 2 ? 4 * q : i;
           R.out_len = 3 * q;
           return R;
@@ -447,7 +451,7 @@ __device__ __forceinline__ StreamResult finish_stream(const uint8_t *c, int64_t 
     }
   } else {
     int32_t p = 0;
-    if (final_stream && q > 0 && c[m - 1] == '=') p = (c[m - 2] == '=') ? 2 : 1;
+    if (final_stream && q > 0 && c(m - 1) == '=') p = (c(m - 2) == '=') ? 2 : 1;
     R.pad_count = p;
     R.out_len = 3 * q - p;
     if (p == 2) {
@@ -460,12 +464,18 @@ __device__ __forceinline__ StreamResult finish_stream(const uint8_t *c, int64_t 
   }
   R.status = 0;
   R.err_pos = -1;
-  if ((flags & kFlagStrict) && last >= 0 && (g_dec_tab[c[last]] * shift) % 256 != 0) {
+  if ((flags & kFlagStrict) && last >= 0 && (g_dec_tab[c(last)] * shift) % 256 != 0) {
     R.status = 3;
     R.err_pos = last;
     R.out_len = 3 * (last / 4);
     R.pad_count = 0;
   }
   return R;
+}
+
+__device__ __forceinline__ StreamResult finish_stream(const uint8_t *c, int64_t m, uint8_t *out,
+                                                      int64_t err, bool final_stream, int flags) {
+  return finish_stream_at([c](int64_t i) -> uint32_t { return c[i]; }, m, out, err, final_stream,
+                          flags);
 }
 }  // namespace b64

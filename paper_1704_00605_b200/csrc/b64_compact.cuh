@@ -1,0 +1,313 @@
+// b64_compact.cuh -- whitespace compaction on the GPU: Appendix B whitespace
+// removal and the compaction front end of the fused
+// whitespace-tolerant decode (row f4, b64_ws.cuh).  Removed bytes: ' ' (0x20),
+// '\n' (0x0A), '\r' (0x0D) (hex codes per reading G8).
+//
+// The paper's SSE kernel compacts 16 bytes with a 65,536-entry shuffle table
+// (P:1250-1271); a GPU has no byte shuffle across a register file, but it has
+// a conflict-free byte gather/scatter in shared memory and warp ballots /
+// shuffles.  Layout: the input is cut into 16 KiB tiles aligned to 16-byte
+// granules of HBM (tile t = window [a0 + t*16K, a0 + (t+1)*16K), a0 = d_in
+// rounded down to 16 B; the first and last tiles are partial); consecutive
+// tiles form one chunk per CTA.  Two kernels:
+//   cp_count_kernel   kept bytes per chunk (16-byte coalesced loads, SWAR test)
+//   <consumer>        per chunk, at the offset given by the counts of the
+//                     chunks before it: TMA-stage each tile, compact it into a
+//                     shared-memory stream (compact_tile), consume the stream
+//                     (copy-out for despace, base64 decode for the fused path).
+// compact_tile: warp w owns the tile's words [256w, 256w+256); lane l reads
+// words 32i + l (i = 0..7, conflict-free LDS.32), keeps a 4-bit keep mask
+// per word (8 nibbles in one register), scans the per-word counts of the
+// warp with one packed-byte shuffle scan (4 counts per register, 2
+// registers), block-scans the 16 warp totals and places every kept byte
+// with a predicated STS.U8 (consecutive lanes -> consecutive words, no bank
+// conflicts).  Order is preserved.
+#pragma once
+#include <cstdint>
+
+#include "b64_batch.cuh"
+#include "b64_codec.cuh"
+#include "b64_ptx.cuh"
+
+namespace b64 {
+
+constexpr int kCpWarps = 16;
+constexpr int kCpThreads = kCpWarps * 32;
+constexpr int kCpTile = 16384;                      // input window bytes per tile
+constexpr int kCpWords = kCpTile / 4;               // 4096 words
+constexpr int kCpWarpWords = kCpWords / kCpWarps;   // 256 words = 1 KiB per warp
+constexpr int kCpPerLane = kCpWarpWords / 32;       // 8 words per lane
+static_assert(kCpPerLane == 8, "compact_tile packs 8 keep nibbles per lane");
+constexpr int kCpStages = 3;                        // TMA input ring depth
+constexpr int kCpCtasPerSm = 2;
+constexpr int kCpMaxChunks = 4096;
+
+// Per-byte keep flags: bit 7 of each byte of the result is set iff that byte
+// of w is NOT one of 0x20, 0x0A, 0x0D.  (x ^ K) & 0x7F + 0x7F has bit 7 set
+// iff the low 7 bits of x differ from K (no carry leaves a byte: at most
+// 0x7F + 0x7F); bytes >= 0x80 are always kept.  8 ALU ops per word.
+__device__ __forceinline__ uint32_t keep_flags(uint32_t w) {
+  const uint32_t s1 = ((w ^ 0x20202020u) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+  const uint32_t s2 = ((w ^ 0x0A0A0A0Au) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+  const uint32_t s3 = ((w ^ 0x0D0D0D0Du) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+  return ((s1 & s2 & s3) | w) & 0x80808080u;
+}
+
+// Bits 7, 15, 23, 31 of f -> bits 0..3 (one multiply: the four partial
+// products land on distinct bits 28..31).
+__device__ __forceinline__ uint32_t gather4(uint32_t f) { return (f * 0x00204081u) >> 28; }
+
+__device__ __forceinline__ bool is_space_byte(uint32_t v) {
+  return v == 0x20u || v == 0x0Au || v == 0x0Du;
+}
+
+// Kept-byte count of one 16-byte granule whose valid bytes are [lo, hi).
+__device__ __forceinline__ int kept_granule(const uint4 &v, int lo, int hi) {
+  uint32_t k = gather4(keep_flags(v.x)) | gather4(keep_flags(v.y)) << 4 |
+               gather4(keep_flags(v.z)) << 8 | gather4(keep_flags(v.w)) << 12;
+  const uint32_t vm = (hi >= 16 ? 0xFFFFu : (1u << hi) - 1u) & ~((1u << lo) - 1u);
+  return __popc(k & vm);
+}
+
+// ------------------------------------------------------------ geometry ---
+struct CpGeom {
+  const uint8_t *in;  // d_in
+  uintptr_t a0;       // d_in rounded down to 16 bytes
+  int imis;           // d_in - a0
+  int64_t m;          // input bytes
+  int64_t ntiles;     // ceil((imis + m) / kCpTile)
+  int64_t tpc;        // tiles per chunk
+  __device__ __forceinline__ void init(const uint8_t *p, int64_t m_, int64_t tpc_) {
+    in = p;
+    a0 = reinterpret_cast<uintptr_t>(p) & ~static_cast<uintptr_t>(15);
+    imis = static_cast<int>(reinterpret_cast<uintptr_t>(p) & 15);
+    m = m_;
+    ntiles = (imis + m + kCpTile - 1) / kCpTile;
+    tpc = tpc_;
+  }
+  // valid window bytes of tile t: [lo, hi)
+  __device__ __forceinline__ int lo(int64_t t) const { return t == 0 ? imis : 0; }
+  __device__ __forceinline__ int hi(int64_t t) const {
+    const int64_t h = imis + m - t * kCpTile;
+    return h < kCpTile ? static_cast<int>(h) : kCpTile;
+  }
+  // input offset (relative to d_in) of window byte x of tile t
+  __device__ __forceinline__ int64_t off(int64_t t, int x) const { return t * kCpTile + x - imis; }
+};
+
+// Pass 1: kept bytes of chunk b = tiles [b*tpc, (b+1)*tpc).  reset (may be
+// null): two words of a consumer's scratch set to {~0, 0} for the launch that
+// follows on the same stream.
+__global__ void __launch_bounds__(kCpThreads)
+    cp_count_kernel(const uint8_t *__restrict__ in, int64_t m, int64_t tpc,
+                    int64_t *__restrict__ counts, unsigned long long *reset) {
+  __shared__ int64_t sh[66];
+  if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    reset[0] = ~0ull;
+    reset[1] = 0ull;
+  }
+  CpGeom G;
+  G.init(in, m, tpc);
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tpc;
+  const int64_t t1 = t0 + tpc < G.ntiles ? t0 + tpc : G.ntiles;
+  // window bytes [W0, W1) relative to a0; valid bytes [imis, imis + m)
+  const int64_t W0 = t0 * kCpTile;
+  const int64_t W1 = t1 * kCpTile < G.imis + m ? t1 * kCpTile : G.imis + m;
+  int64_t g0 = W0 / 16, g1 = (W1 + 15) / 16;  // granules of the chunk
+  int cnt = 0;
+  const uint4 *q = reinterpret_cast<const uint4 *>(G.a0);
+  // peel the partial first / last granule of the whole input
+  if (blockIdx.x == 0 && G.imis != 0) {
+    if (threadIdx.x == 0) cnt += kept_granule(q[0], G.imis, W1 - 0 < 16 ? static_cast<int>(W1) : 16);
+    ++g0;
+  }
+  if (g1 > g0 && (W1 & 15) != 0) {
+    --g1;
+    if (threadIdx.x == 0) cnt += kept_granule(q[g1], 0, static_cast<int>(W1 & 15));
+  }
+  int64_t i = g0 + threadIdx.x;
+  for (; i + 3 * kCpThreads < g1; i += 4 * kCpThreads) {
+    const uint4 a = __ldcs(q + i), b = __ldcs(q + i + kCpThreads);
+    const uint4 c = __ldcs(q + i + 2 * kCpThreads), d = __ldcs(q + i + 3 * kCpThreads);
+    cnt += kept_granule(a, 0, 16) + kept_granule(b, 0, 16) + kept_granule(c, 0, 16) +
+           kept_granule(d, 0, 16);
+  }
+  for (; i < g1; i += kCpThreads) cnt += kept_granule(__ldcs(q + i), 0, 16);
+  int64_t p, pb, tot, tb;
+  block_exclusive_scan2(cnt, 0, p, pb, tot, tb, sh);
+  if (threadIdx.x == 0) counts[blockIdx.x] = tot;
+}
+
+// Sum of counts[0..b) and of all counts[0..n) (every thread gets both).
+__device__ __forceinline__ void chunk_prefix(const int64_t *counts, int64_t n, int64_t b,
+                                             int64_t &before, int64_t &total, int64_t *sh) {
+  int64_t x = 0, y = 0;
+  for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+    const int64_t v = counts[c];
+    y += v;
+    if (c < b) x += v;
+  }
+  int64_t p, pb;
+  block_exclusive_scan2(x, y, p, pb, before, total, sh);
+}
+
+// Shared memory of a compaction consumer CTA.
+struct alignas(128) CpSmem {
+  uint8_t win[kCpStages][kCpTile];  // TMA ring (16-byte aligned windows)
+  uint64_t full[kCpStages];
+  int32_t wcnt[kCpWarps];
+};
+
+// Issue the bulk load of tile t into ring slot s (one thread).
+__device__ __forceinline__ void cp_load(CpSmem &S, const CpGeom &G, int64_t t, int s,
+                                        uint64_t pol) {
+  const int h = G.hi(t);
+  const uint32_t bytes = static_cast<uint32_t>((h + 15) & ~15);
+  ptx::mbar_arrive_expect_tx(&S.full[s], bytes);
+  ptx::bulk_g2s(S.win[s], reinterpret_cast<const void *>(G.a0 + static_cast<uintptr_t>(t) * kCpTile),
+                bytes, &S.full[s], pol);
+}
+
+// Keep mask of the 4 bytes of window word wi restricted to [lo, hi).
+__device__ __forceinline__ uint32_t valid4(int lo, int hi, int wi) {
+  const int a = lo - 4 * wi, b = hi - 4 * wi;
+  const uint32_t top = b >= 4 ? 0xFu : b <= 0 ? 0u : (1u << b) - 1u;
+  const uint32_t bot = a <= 0 ? 0u : a >= 4 ? 0xFu : (1u << a) - 1u;
+  return top & ~bot;
+}
+
+// Compact the valid bytes [lo, hi) of a 16 KiB window (smem, 16-byte
+// aligned) into stream[dst, dst + n), in order; returns n (all threads).
+// Contains one __syncthreads; the caller synchronises before reading the
+// stream.  EDGE: lo != 0 or hi != kCpTile.
+template <bool EDGE>
+__device__ __forceinline__ int compact_tile(const uint8_t *win, int lo, int hi, uint8_t *stream,
+                                            int dst, int32_t *wcnt) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t *seg = reinterpret_cast<const uint32_t *>(win) + warp * kCpWarpWords + lane;
+  uint32_t nib = 0;
+#pragma unroll
+  for (int i = 0; i < kCpPerLane; ++i) {
+    uint32_t k = gather4(keep_flags(seg[32 * i]));
+    if (EDGE) k &= valid4(lo, hi, warp * kCpWarpWords + 32 * i + lane);
+    nib |= k << (4 * i);
+  }
+  // per-word kept counts (nibble popcounts), 4 per register as bytes
+  uint32_t nc = nib - ((nib >> 1) & 0x55555555u);
+  nc = (nc & 0x33333333u) + ((nc >> 2) & 0x33333333u);
+  const uint32_t x0 = nc & 0x0F0F0F0Fu;         // words 0, 2, 4, 6
+  const uint32_t x1 = (nc >> 4) & 0x0F0F0F0Fu;  // words 1, 3, 5, 7
+  uint32_t s0 = x0, s1 = x1;                    // inclusive scans (bytes <= 128)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u0 = __shfl_up_sync(0xffffffffu, s0, o);
+    const uint32_t u1 = __shfl_up_sync(0xffffffffu, s1, o);
+    if (lane >= o) {
+      s0 += u0;
+      s1 += u1;
+    }
+  }
+  const uint32_t T0 = __shfl_sync(0xffffffffu, s0, 31), T1 = __shfl_sync(0xffffffffu, s1, 31);
+  const uint32_t e0 = s0 - x0, e1 = s1 - x1;  // exclusive, per byte
+  // warp total = sum of the 8 bytes of T0, T1
+  const uint32_t h = (T0 & 0x00FF00FFu) + ((T0 >> 8) & 0x00FF00FFu) + (T1 & 0x00FF00FFu) +
+                     ((T1 >> 8) & 0x00FF00FFu);
+  const int wtot = static_cast<int>((h & 0xFFFFu) + (h >> 16));
+  if (lane == 0) wcnt[warp] = wtot;
+  __syncthreads();
+  const int c = lane < kCpWarps ? wcnt[lane] : 0;
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < kCpWarps; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  const int wpre = __shfl_sync(0xffffffffu, incl - c, warp);
+  const int total = __shfl_sync(0xffffffffu, incl, kCpWarps - 1);
+  uint8_t *ws = stream + dst + wpre;
+  int base = 0;  // kept bytes of this warp's words 32*i' + *, i' < i
+#pragma unroll
+  for (int i = 0; i < kCpPerLane; ++i) {
+    const uint32_t w = seg[32 * i];
+    const uint32_t k = (nib >> (4 * i)) & 0xFu;
+    const uint32_t E = (i & 1) ? e1 : e0, T = (i & 1) ? T1 : T0;
+    const int sh = 8 * (i >> 1);
+    uint8_t *p = ws + base + static_cast<int>((E >> sh) & 0xFFu);
+    if (k & 1u) p[0] = static_cast<uint8_t>(w);
+    if (k & 2u) p[k & 1u] = static_cast<uint8_t>(w >> 8);
+    if (k & 4u) p[__popc(k & 3u)] = static_cast<uint8_t>(w >> 16);
+    if (k & 8u) p[__popc(k & 7u)] = static_cast<uint8_t>(w >> 24);
+    base += static_cast<int>((T >> sh) & 0xFFu);
+  }
+  return total;
+}
+
+// CTA-wide copy of n bytes from smem src to global dst, where src and dst
+// are congruent mod 16: aligned LDS.128 -> STG.128 for the interior, byte
+// stores for the (< 16 byte) edges.
+__device__ __forceinline__ void cta_copy_out_congruent(uint8_t *dst, const uint8_t *src, int n) {
+  const int tid = threadIdx.x;
+  const uintptr_t g = reinterpret_cast<uintptr_t>(dst);
+  const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
+  const uintptr_t a1 = (g + static_cast<uintptr_t>(n)) & ~static_cast<uintptr_t>(15);
+  if (a1 > a0) {
+    const int head = static_cast<int>(a0 - g);
+    const int ng = static_cast<int>((a1 - a0) >> 4);
+    for (int q = tid; q < ng; q += blockDim.x)
+      *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a0) + 16 * q) =
+          *reinterpret_cast<const uint4 *>(src + head + 16 * q);
+    const int tail0 = static_cast<int>(a1 - g);
+    if (tid < head) dst[tid] = src[tid];
+    if (tid >= 32 && tid - 32 < n - tail0) dst[tail0 + tid - 32] = src[tail0 + tid - 32];
+  } else if (tid < n) {
+    dst[tid] = src[tid];
+  }
+}
+
+// ------------------------------------------------------ despace (f3) ---
+struct alignas(128) DsSmem {
+  CpSmem cp;
+  uint8_t stream[kCpTile + 32];
+  int64_t red[66];
+};
+
+__global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
+    despace_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
+                   const int64_t *__restrict__ counts, int64_t tpc, int64_t *out_len) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  DsSmem &S = *reinterpret_cast<DsSmem *>(smem_raw);
+  const int tid = threadIdx.x;
+  CpGeom G;
+  G.init(in, m, tpc);
+  if (tid == 0) {
+    for (int s = 0; s < kCpStages; ++s) ptx::mbar_init(&S.cp.full[s], 1);
+    ptx::fence_mbar_init();
+  }
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tpc;
+  const int64_t t1 = t0 + tpc < G.ntiles ? t0 + tpc : G.ntiles;
+  int64_t running, total;
+  chunk_prefix(counts, gridDim.x, blockIdx.x, running, total, S.red);  // has a __syncthreads
+  const uint64_t pol = ptx::policy_evict_first();
+  if (tid == 0)
+    for (int s = 0; s < kCpStages - 1 && t0 + s < t1; ++s) cp_load(S.cp, G, t0 + s, s, pol);
+  const uintptr_t obase = reinterpret_cast<uintptr_t>(out);
+  for (int64_t t = t0; t < t1; ++t) {
+    const int it = static_cast<int>(t - t0);
+    const int s = it % kCpStages;
+    if (tid == 0 && t + kCpStages - 1 < t1)
+      cp_load(S.cp, G, t + kCpStages - 1, (it + kCpStages - 1) % kCpStages, pol);
+    ptx::mbar_wait_spin(&S.cp.full[s], static_cast<uint32_t>((it / kCpStages) & 1));
+    const int lo = G.lo(t), hi = G.hi(t);
+    const int dst = static_cast<int>((obase + static_cast<uintptr_t>(running)) & 15);
+    const int n = (lo != 0 || hi != kCpTile)
+                      ? compact_tile<true>(S.cp.win[s], lo, hi, S.stream, dst, S.cp.wcnt)
+                      : compact_tile<false>(S.cp.win[s], lo, hi, S.stream, dst, S.cp.wcnt);
+    ptx::fence_proxy_async_smem();  // generic reads of win[s] before its next bulk write
+    __syncthreads();
+    cta_copy_out_congruent(out + running, S.stream + dst, n);
+    running += n;
+  }
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) *out_len = total;
+}
+
+}  // namespace b64

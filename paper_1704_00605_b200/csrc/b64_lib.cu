@@ -22,7 +22,8 @@
 #include "b64_codec.cuh"
 #include "b64_ptx.cuh"
 #include "b64_batch.cuh"
-#include "b64_despace.cuh"
+#include "b64_compact.cuh"
+#include "b64_ws.cuh"
 
 namespace b64 {
 
@@ -365,6 +366,7 @@ bool device_setup(int *dev_out, int *sms_out) {
         if (set_smem(f, sizeof(DecSmem)) != cudaSuccess) return false;
     if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return false;
     if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return false;
+    if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return false;
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return false;
     di.attrs_set = true;
   }
@@ -722,9 +724,21 @@ int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out
   return B64_OK;
 }
 
+// Chunking of the compaction kernels: one chunk of consecutive 16 KiB tiles
+// per CTA, kCpCtasPerSm CTAs per SM, at most kCpMaxChunks chunks.
+static void cp_plan(const void *d_in, int64_t m, int sms, int64_t *ntiles, int64_t *tpc,
+                    int64_t *grid) {
+  const int64_t imis = static_cast<int64_t>(reinterpret_cast<uintptr_t>(d_in) & 15);
+  *ntiles = (imis + m + kCpTile - 1) / kCpTile;
+  int64_t ctas = static_cast<int64_t>(sms) * kCpCtasPerSm;
+  if (ctas > kCpMaxChunks) ctas = kCpMaxChunks;
+  *tpc = (*ntiles + ctas - 1) / ctas;
+  *grid = (*ntiles + *tpc - 1) / *tpc;
+}
+
 size_t b64_despace_workspace_bytes(int64_t m) {
   if (m < 0) return 0;
-  return 8 * 4096;  // per-chunk kept counts (<= 4096 chunks)
+  return 8 * kCpMaxChunks;  // per-chunk kept counts
 }
 
 int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_len, void *d_ws,
@@ -738,17 +752,65 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
                                                                                  : B64_ERR_CUDA;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
-  const int64_t ntiles = (m + kDsTile - 1) / kDsTile;
-  int64_t ctas = static_cast<int64_t>(sms) * kDsCtasPerSm;
-  if (ctas > 4096) ctas = 4096;
-  const int64_t tpc = (ntiles + ctas - 1) / ctas;    // tiles per chunk
-  const int64_t grid = (ntiles + tpc - 1) / tpc;      // chunks
+  int64_t ntiles, tpc, grid;
+  cp_plan(d_in, m, sms, &ntiles, &tpc, &grid);
   int64_t *counts = static_cast<int64_t *>(d_ws);
-  despace_count_kernel<<<static_cast<unsigned>(grid), kDsThreads, 0, stream>>>(d_in, m, tpc,
-                                                                                counts);
-  despace_kernel<<<static_cast<unsigned>(grid), kDsThreads, sizeof(DsSmem), stream>>>(
-      d_in, m, d_out, counts, tpc, d_out_len, ntiles);
+  cp_count_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(d_in, m, tpc, counts,
+                                                                           nullptr);
+  despace_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(DsSmem), stream>>>(
+      d_in, m, d_out, counts, tpc, d_out_len);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
+}
+
+size_t b64_decode_ws_workspace_bytes(int64_t m) {
+  if (m < 0) return 0;
+  const int64_t ntiles = (15 + m + kCpTile - 1) / kCpTile;
+  return kWsHdrBytes + 8 * kCpMaxChunks + 4 * static_cast<size_t>(ntiles);
+}
+
+int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
+                        b64_result *d_result, void *d_ws, size_t ws_bytes, b64_stream_t stream) {
+  if (m < 0 || !flags_ok(flags) || d_result == nullptr || (m > 0 && d_in == nullptr) ||
+      (b64_decoded_max_len_ex(m, flags) > 0 && d_out == nullptr))
+    return B64_ERR_ARG;
+  if (m == 0) {
+    const b64_result r{0, -1, B64_OK, 0};
+    return cudaMemcpyAsync(d_result, &r, sizeof(r), cudaMemcpyHostToDevice, stream) == cudaSuccess
+               ? B64_OK
+               : B64_ERR_CUDA;
+  }
+  if (d_ws == nullptr || ws_bytes < b64_decode_ws_workspace_bytes(m) ||
+      (reinterpret_cast<uintptr_t>(d_ws) & 15) != 0)
+    return B64_ERR_WORKSPACE;
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  int64_t ntiles, tpc, grid;
+  cp_plan(d_in, m, sms, &ntiles, &tpc, &grid);
+  uint8_t *base = static_cast<uint8_t *>(d_ws);
+  WsHdr *hdr = reinterpret_cast<WsHdr *>(base);
+  int64_t *counts = reinterpret_cast<int64_t *>(base + kWsHdrBytes);
+  int32_t *tcnt = reinterpret_cast<int32_t *>(base + kWsHdrBytes + 8 * kCpMaxChunks);
+  cp_count_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(
+      d_in, m, tpc, counts, &hdr->errkey);
+  decode_ws_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(WsSmem), stream>>>(
+      d_in, m, d_out, counts, tcnt, tpc, hdr, d_result, flags);
+  return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
+}
+
+int b64_decode_ws(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int64_t *out_len,
+                  int64_t *err_pos, void *d_ws, size_t ws_bytes, b64_stream_t stream) {
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  StreamWs *w = stream_ws(dev, stream);
+  if (w == nullptr) return B64_ERR_CUDA;
+  const int rc = b64_decode_ws_async(d_in, m, d_out, flags, w->d_res, d_ws, ws_bytes, stream);
+  if (rc != B64_OK) return rc;
+  if (cudaStreamSynchronize(stream) != cudaSuccess) return B64_ERR_CUDA;
+  b64_result r;
+  std::memcpy(&r, w->h_res, sizeof(r));
+  if (out_len) *out_len = r.out_len;
+  if (err_pos) *err_pos = r.err_pos;
+  return r.status;
 }
 
 int b64_shard(int64_t total, int unit, int world, int rank, int64_t *begin, int64_t *end) {

@@ -1,0 +1,159 @@
+"""GPU parity of the fused whitespace-tolerant decode (SURVEY.md §8(f) row f4,
+reading R-ws-decode) against oracle.decode_ws: MIME-wrapped text across tile
+(16 KiB) and chunk seams, random whitespace densities, whitespace-only
+chunks, long whitespace runs, every error kind with its offset in ORIGINAL
+coordinates, the variant flags, in/out misalignment and guard bytes."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1704_00605_b200 as b64
+from inputs.gen import splitmix_bytes
+from tests.gpu_util import empty_dev, host, to_dev
+
+pytestmark = pytest.mark.gpu
+TILE = 16384
+U, NP, ST = b64.B64_FLAG_URL, b64.B64_FLAG_NOPAD, b64.B64_FLAG_STRICT
+WS = np.frombuffer(b" \n\r", dtype=np.uint8)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    b64.load_library()
+
+
+def gpu(w, fl=0, im=0, om=0):
+    cap = b64.b64_decoded_max_len_ex(w.size, fl)
+    base, out = empty_dev(cap, om)
+    view, st, ep = b64.b64_decode_ws(to_dev(w, im), out=out, flags=fl)
+    g = host(base)
+    assert (g[:om] == 0xCC).all() and (g[om + cap:] == 0xCC).all(), "guard bytes"
+    return st, ep, host(view)
+
+
+def check(w, fl=0, im=0, om=0):
+    st, ep, out = gpu(w, fl, im, om)
+    rst, rep, rout = oracle.decode_ws(w, fl)
+    assert (st, ep) == (rst, rep), (w.size, fl, im, om, st, ep, rst, rep)
+    assert out.size == rout.size and np.array_equal(out, rout), (w.size, fl, im, om)
+
+
+def mime(n, seed, line=76, crlf=True, fl=0):
+    return oracle.encode_wrapped(splitmix_bytes(seed, 0, n), line, crlf=crlf, flags=fl)
+
+
+def sprinkle(t, seed, frac):
+    """Insert whitespace runs (1-3 bytes) before a fraction of t's bytes."""
+    rng = np.random.default_rng(seed)
+    k = t.size
+    runs = (rng.random(k) < frac) * rng.integers(1, 4, k)
+    out = np.empty(k + int(runs.sum()), dtype=np.uint8)
+    pos = np.arange(k) + np.cumsum(runs)
+    out[pos] = t
+    mask = np.ones(out.size, dtype=bool)
+    mask[pos] = False
+    out[mask] = rng.choice(WS, size=int(mask.sum()))
+    return out
+
+
+def test_mime_sizes_across_seams():
+    sizes = [0, 1, 2, 3, 56, 57, 58, 12_000, 12_285, 12_288, 12_300, 40_000, 300_001,
+             1_000_000, 3_600_000]
+    for n in sizes:
+        for crlf in (True, False):
+            check(mime(n, 400 + n % 13, crlf=crlf))
+
+
+def test_large_multi_tile_chunks():
+    # > 296 tiles: chunks hold several tiles (carry across tiles inside a chunk)
+    for n, seed in [(9_000_001, 401), (15_728_640, 402)]:
+        check(mime(n, seed))
+        check(mime(n, seed, line=64, crlf=False))
+
+
+@pytest.mark.parametrize("frac", [0.0, 0.01, 0.3, 2.0])
+def test_random_whitespace_densities(frac):
+    x = splitmix_bytes(403, 0, 200_000)
+    t = oracle.encode(x)
+    for k, n in enumerate([4, 5, 16, 17, 100, 4_096, 16_383, 49_153, t.size]):
+        tt = t[:n] if n % 4 == 0 or n == t.size else t[:n]
+        w = sprinkle(tt, 404 + k, min(frac, 1.0)) if frac else tt.copy()
+        if frac > 1.0:  # heavy: every byte preceded by whitespace
+            w = sprinkle(tt, 404 + k, 1.0)
+        check(w)
+
+
+def test_whitespace_only_chunks_and_long_runs():
+    t = oracle.encode(splitmix_bytes(405, 0, 30_000))
+    blank = np.full(5 * TILE + 123, ord(" "), dtype=np.uint8)
+    blank[::7] = ord("\n")
+    # data, a long blank stretch (whole empty tiles / chunks), data, trailing blanks
+    w = np.concatenate([t[:10_001], blank, t[10_001:], blank[:3 * TILE]])
+    check(w)
+    check(blank)  # whitespace only: OK, 0 bytes
+    check(np.concatenate([blank, t[:8]]))
+    check(np.concatenate([t[:5], blank, t[5:8]]))  # a quad split by 80 KiB of blanks
+
+
+def test_alignments():
+    w = mime(120_000, 406)
+    for im in range(0, 16, 3):
+        for om in (0, 1, 4, 7, 12):
+            check(w, 0, im, om)
+
+
+def test_errors_in_original_coordinates():
+    rng = np.random.default_rng(407)
+    na = np.array([b for b in range(256) if b not in b" \n\r=" and oracle.A(b) < 0], dtype=np.uint8)
+    base_w = mime(200_000, 408)
+    for trial in range(60):
+        w = base_w.copy()
+        kind = trial % 4
+        if kind == 0:  # one invalid byte somewhere
+            w[int(rng.integers(0, w.size))] = na[int(rng.integers(0, na.size))]
+        elif kind == 1:  # several invalid bytes
+            for p in rng.choice(w.size, 5, replace=False):
+                w[int(p)] = na[int(rng.integers(0, na.size))]
+        elif kind == 2:  # a '=' in the middle
+            p = int(rng.integers(0, w.size - 100))
+            w[p] = ord("=")
+        else:  # truncated stream (LENGTH, reported at a kept byte)
+            w = w[: int(rng.integers(1, w.size))]
+        check(w)
+
+
+@pytest.mark.parametrize("fl", [U, NP, ST, U | NP | ST])
+def test_variant_flags(fl):
+    rng = np.random.default_rng(409)
+    for n in [0, 1, 2, 3, 4, 5, 1000, 57 * 300 + 1, 57 * 300 + 2, 250_000]:
+        w = mime(n, 410 + n % 7, fl=fl & ~ST)
+        check(w, fl)
+        if n and fl & ST:
+            # break canonicity of the last data character (App. A)
+            t = oracle.encode_ex(splitmix_bytes(411, 0, n), fl & ~ST)
+            if t[-1] == ord("=") or (fl & NP and n % 3):
+                j = t.size - 1
+                while t[j] == ord("="):
+                    j -= 1
+                t = t.copy()
+                t[j] ^= 1
+                check(sprinkle(t, 412, 0.05), fl)
+        if n > 10:
+            w2 = w.copy()
+            w2[int(rng.integers(0, w2.size))] = ord("!")
+            check(w2, fl)
+
+
+def test_async_result_record():
+    w = mime(50_000, 413)
+    d = to_dev(w)
+    out = torch.empty(b64.b64_decoded_max_len(w.size), dtype=torch.uint8, device=d.device)
+    res = b64.result_tensor(d.device)
+    b64.b64_decode_ws_async(d, out, res)
+    ol, ep, st, pc = b64.unpack_result(res)
+    rst, rep, rout = oracle.decode_ws(w)
+    assert (st, ep, ol) == (rst, rep, rout.size)
+    assert np.array_equal(host(out[:ol]), rout)
