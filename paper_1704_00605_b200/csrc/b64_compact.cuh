@@ -46,10 +46,15 @@ constexpr int kCpMaxChunks = 4096;
 // of w is NOT one of 0x20, 0x0A, 0x0D.  (x ^ K) & 0x7F + 0x7F has bit 7 set
 // iff the low 7 bits of x differ from K (no carry leaves a byte: at most
 // 0x7F + 0x7F); bytes >= 0x80 are always kept.  8 ALU ops per word.
+__device__ __forceinline__ uint32_t xor_and7f(uint32_t w, uint32_t K) {  // (w ^ K) & 0x7F7F7F7F
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(d) : "r"(w), "r"(K), "r"(0x7F7F7F7Fu));
+  return d;
+}
 __device__ __forceinline__ uint32_t keep_flags(uint32_t w) {
-  const uint32_t s1 = ((w ^ 0x20202020u) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
-  const uint32_t s2 = ((w ^ 0x0A0A0A0Au) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
-  const uint32_t s3 = ((w ^ 0x0D0D0D0Du) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+  const uint32_t s1 = xor_and7f(w, 0x20202020u) + 0x7F7F7F7Fu;
+  const uint32_t s2 = xor_and7f(w, 0x0A0A0A0Au) + 0x7F7F7F7Fu;
+  const uint32_t s3 = xor_and7f(w, 0x0D0D0D0Du) + 0x7F7F7F7Fu;
   return ((s1 & s2 & s3) | w) & 0x80808080u;
 }
 
@@ -67,6 +72,10 @@ __device__ __forceinline__ int kept_granule(const uint4 &v, int lo, int hi) {
                gather4(keep_flags(v.z)) << 8 | gather4(keep_flags(v.w)) << 12;
   const uint32_t vm = (hi >= 16 ? 0xFFFFu : (1u << hi) - 1u) & ~((1u << lo) - 1u);
   return __popc(k & vm);
+}
+__device__ __forceinline__ int kept_granule_full(const uint4 &v) {
+  return __popc(keep_flags(v.x)) + __popc(keep_flags(v.y)) + __popc(keep_flags(v.z)) +
+         __popc(keep_flags(v.w));
 }
 
 // ------------------------------------------------------------ geometry ---
@@ -95,12 +104,37 @@ struct CpGeom {
   __device__ __forceinline__ int64_t off(int64_t t, int x) const { return t * kCpTile + x - imis; }
 };
 
-// Pass 1: kept bytes of chunk b = tiles [b*tpc, (b+1)*tpc).  reset (may be
-// null): two words of a consumer's scratch set to {~0, 0} for the launch that
-// follows on the same stream.
+// Keep mask of the 4 bytes of window word wi restricted to [lo, hi).
+__device__ __forceinline__ uint32_t valid4(int lo, int hi, int wi) {
+  const int a = lo - 4 * wi, b = hi - 4 * wi;
+  const uint32_t top = b >= 4 ? 0xFu : b <= 0 ? 0u : (1u << b) - 1u;
+  const uint32_t bot = a <= 0 ? 0u : a >= 4 ? 0xFu : (1u << a) - 1u;
+  return top & ~bot;
+}
+
+// Pass 1 (classification): for every tile t and thread slot tid of the
+// consumer (warp w, lane l), the 4-bit keep masks of window words
+// 256w + 32i + l, i = 0..7, packed as 8 nibbles -> masks[t*512 + tid]
+// (exact: bytes outside the input are 0); counts[b] = kept bytes of chunk b
+// = tiles [b*tpc, (b+1)*tpc).  Loads are coalesced 128-byte warp rows, two
+// tiles in flight per thread.  reset (may be null): two words of a
+// consumer's scratch set to {~0, 0} for the launch that follows.
+__device__ __forceinline__ uint32_t tile_nib(const uint32_t (&w)[kCpPerLane], int lo, int hi,
+                                             int wbase, bool edge) {
+  uint32_t nib = 0;
+#pragma unroll
+  for (int i = 0; i < kCpPerLane; ++i) {
+    uint32_t k = gather4(keep_flags(w[i]));
+    if (edge) k &= valid4(lo, hi, wbase + 32 * i);
+    nib |= k << (4 * i);
+  }
+  return nib;
+}
+
 __global__ void __launch_bounds__(kCpThreads)
-    cp_count_kernel(const uint8_t *__restrict__ in, int64_t m, int64_t tpc,
-                    int64_t *__restrict__ counts, unsigned long long *reset) {
+    cp_mask_kernel(const uint8_t *__restrict__ in, int64_t m, int64_t tpc,
+                   int64_t *__restrict__ counts, uint32_t *__restrict__ masks,
+                   unsigned long long *reset) {
   __shared__ int64_t sh[66];
   if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     reset[0] = ~0ull;
@@ -108,34 +142,37 @@ __global__ void __launch_bounds__(kCpThreads)
   }
   CpGeom G;
   G.init(in, m, tpc);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wbase = warp * kCpWarpWords + lane;  // this thread's first window word
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tpc;
   const int64_t t1 = t0 + tpc < G.ntiles ? t0 + tpc : G.ntiles;
-  // window bytes [W0, W1) relative to a0; valid bytes [imis, imis + m)
-  const int64_t W0 = t0 * kCpTile;
-  const int64_t W1 = t1 * kCpTile < G.imis + m ? t1 * kCpTile : G.imis + m;
-  int64_t g0 = W0 / 16, g1 = (W1 + 15) / 16;  // granules of the chunk
   int cnt = 0;
-  const uint4 *q = reinterpret_cast<const uint4 *>(G.a0);
-  // peel the partial first / last granule of the whole input
-  if (blockIdx.x == 0 && G.imis != 0) {
-    if (threadIdx.x == 0) cnt += kept_granule(q[0], G.imis, W1 - 0 < 16 ? static_cast<int>(W1) : 16);
-    ++g0;
+  for (int64_t t = t0; t < t1; t += 2) {
+    const bool two = t + 1 < t1;
+    const uint32_t *wa = reinterpret_cast<const uint32_t *>(G.a0 + static_cast<uintptr_t>(t) * kCpTile);
+    const int lo0 = G.lo(t), hi0 = G.hi(t);
+    const int lo1 = two ? G.lo(t + 1) : 0, hi1 = two ? G.hi(t + 1) : 0;
+    const bool e0 = lo0 != 0 || hi0 != kCpTile, e1 = two && (lo1 != 0 || hi1 != kCpTile);
+    const int lim0 = (hi0 + 15) & ~15, lim1 = (hi1 + 15) & ~15;  // loadable window bytes
+    uint32_t a[kCpPerLane], b[kCpPerLane];
+#pragma unroll
+    for (int i = 0; i < kCpPerLane; ++i) {
+      const int wi = wbase + 32 * i;
+      a[i] = (!e0 || 4 * wi < lim0) ? __ldcs(wa + wi) : 0u;
+      b[i] = two && (!e1 || 4 * wi < lim1) ? __ldcs(wa + kCpWords + wi) : 0u;
+    }
+    const uint32_t na = tile_nib(a, lo0, hi0, wbase, e0);
+    masks[t * kCpThreads + tid] = na;
+    cnt += __popc(na);
+    if (two) {
+      const uint32_t nb = tile_nib(b, lo1, hi1, wbase, e1);
+      masks[(t + 1) * kCpThreads + tid] = nb;
+      cnt += __popc(nb);
+    }
   }
-  if (g1 > g0 && (W1 & 15) != 0) {
-    --g1;
-    if (threadIdx.x == 0) cnt += kept_granule(q[g1], 0, static_cast<int>(W1 & 15));
-  }
-  int64_t i = g0 + threadIdx.x;
-  for (; i + 3 * kCpThreads < g1; i += 4 * kCpThreads) {
-    const uint4 a = __ldcs(q + i), b = __ldcs(q + i + kCpThreads);
-    const uint4 c = __ldcs(q + i + 2 * kCpThreads), d = __ldcs(q + i + 3 * kCpThreads);
-    cnt += kept_granule(a, 0, 16) + kept_granule(b, 0, 16) + kept_granule(c, 0, 16) +
-           kept_granule(d, 0, 16);
-  }
-  for (; i < g1; i += kCpThreads) cnt += kept_granule(__ldcs(q + i), 0, 16);
   int64_t p, pb, tot, tb;
   block_exclusive_scan2(cnt, 0, p, pb, tot, tb, sh);
-  if (threadIdx.x == 0) counts[blockIdx.x] = tot;
+  if (tid == 0) counts[blockIdx.x] = tot;
 }
 
 // Sum of counts[0..b) and of all counts[0..n) (every thread gets both).
@@ -153,45 +190,48 @@ __device__ __forceinline__ void chunk_prefix(const int64_t *counts, int64_t n, i
 
 // Shared memory of a compaction consumer CTA.
 struct alignas(128) CpSmem {
-  uint8_t win[kCpStages][kCpTile];  // TMA ring (16-byte aligned windows)
+  uint8_t win[kCpStages][kCpTile];         // TMA ring (16-byte aligned windows)
+  uint32_t msk[kCpStages][kCpThreads];     // the tiles' keep masks (cp_mask_kernel)
   uint64_t full[kCpStages];
   int32_t wcnt[kCpWarps];
+  uint32_t ktab[16];  // per 4-bit keep mask: PRMT selector (bits 0..15) | (2^c - 1) << 16
 };
 
-// Issue the bulk load of tile t into ring slot s (one thread).
-__device__ __forceinline__ void cp_load(CpSmem &S, const CpGeom &G, int64_t t, int s,
-                                        uint64_t pol) {
+// Fill CpSmem::ktab (threads 0..15); needs a barrier before use.
+__device__ __forceinline__ void init_ktab(uint32_t *ktab) {
+  const int k = threadIdx.x;
+  if (k < 16) {
+    uint32_t sel = 0x4444u, c = 0;  // unused slots select a zero byte
+    for (int j = 0; j < 4; ++j)
+      if (k & (1 << j)) {
+        sel = (sel & ~(0xFu << (4 * c))) | (static_cast<uint32_t>(j) << (4 * c));
+        ++c;
+      }
+    ktab[k] = sel | (((1u << c) - 1u) << 16);
+  }
+}
+
+// Issue the bulk loads of tile t (window + keep masks) into ring slot s (one thread).
+__device__ __forceinline__ void cp_load(CpSmem &S, const CpGeom &G, const uint32_t *masks,
+                                        int64_t t, int s, uint64_t pol) {
   const int h = G.hi(t);
   const uint32_t bytes = static_cast<uint32_t>((h + 15) & ~15);
-  ptx::mbar_arrive_expect_tx(&S.full[s], bytes);
+  ptx::mbar_arrive_expect_tx(&S.full[s], bytes + 4 * kCpThreads);
   ptx::bulk_g2s(S.win[s], reinterpret_cast<const void *>(G.a0 + static_cast<uintptr_t>(t) * kCpTile),
                 bytes, &S.full[s], pol);
+  ptx::bulk_g2s(S.msk[s], masks + t * kCpThreads, 4 * kCpThreads, &S.full[s], pol);
 }
 
-// Keep mask of the 4 bytes of window word wi restricted to [lo, hi).
-__device__ __forceinline__ uint32_t valid4(int lo, int hi, int wi) {
-  const int a = lo - 4 * wi, b = hi - 4 * wi;
-  const uint32_t top = b >= 4 ? 0xFu : b <= 0 ? 0u : (1u << b) - 1u;
-  const uint32_t bot = a <= 0 ? 0u : a >= 4 ? 0xFu : (1u << a) - 1u;
-  return top & ~bot;
-}
-
-// Compact the valid bytes [lo, hi) of a 16 KiB window (smem, 16-byte
-// aligned) into stream[dst, dst + n), in order; returns n (all threads).
-// Contains one __syncthreads; the caller synchronises before reading the
-// stream.  EDGE: lo != 0 or hi != kCpTile.
-template <bool EDGE>
-__device__ __forceinline__ int compact_tile(const uint8_t *win, int lo, int hi, uint8_t *stream,
-                                            int dst, int32_t *wcnt) {
+// Compact the kept bytes of a 16 KiB window (smem, 16-byte aligned; keep
+// masks msk[tid] from cp_mask_kernel) into stream[dst, dst + n), in order;
+// returns n (all threads).  Contains one __syncthreads; the caller
+// synchronises before reading the stream.
+__device__ __forceinline__ int compact_tile(const uint8_t *win, const uint32_t *msk,
+                                            uint8_t *stream, int dst, int32_t *wcnt,
+                                            const uint32_t *ktab) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t *seg = reinterpret_cast<const uint32_t *>(win) + warp * kCpWarpWords + lane;
-  uint32_t nib = 0;
-#pragma unroll
-  for (int i = 0; i < kCpPerLane; ++i) {
-    uint32_t k = gather4(keep_flags(seg[32 * i]));
-    if (EDGE) k &= valid4(lo, hi, warp * kCpWarpWords + 32 * i + lane);
-    nib |= k << (4 * i);
-  }
+  const uint32_t nib = msk[tid];
   // per-word kept counts (nibble popcounts), 4 per register as bytes
   uint32_t nc = nib - ((nib >> 1) & 0x55555555u);
   nc = (nc & 0x33333333u) + ((nc >> 2) & 0x33333333u);
@@ -228,15 +268,17 @@ __device__ __forceinline__ int compact_tile(const uint8_t *win, int lo, int hi, 
   int base = 0;  // kept bytes of this warp's words 32*i' + *, i' < i
 #pragma unroll
   for (int i = 0; i < kCpPerLane; ++i) {
-    const uint32_t w = seg[32 * i];
-    const uint32_t k = (nib >> (4 * i)) & 0xFu;
+    // the word's kept bytes, packed low by one PRMT, stored at p[0..c)
+    const uint32_t e = ktab[(nib >> (4 * i)) & 0xFu];
+    uint32_t cw;  // PRMT reads only the selector's low 16 bits
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(cw) : "r"(seg[32 * i]), "r"(e));
     const uint32_t E = (i & 1) ? e1 : e0, T = (i & 1) ? T1 : T0;
     const int sh = 8 * (i >> 1);
     uint8_t *p = ws + base + static_cast<int>((E >> sh) & 0xFFu);
-    if (k & 1u) p[0] = static_cast<uint8_t>(w);
-    if (k & 2u) p[k & 1u] = static_cast<uint8_t>(w >> 8);
-    if (k & 4u) p[__popc(k & 3u)] = static_cast<uint8_t>(w >> 16);
-    if (k & 8u) p[__popc(k & 7u)] = static_cast<uint8_t>(w >> 24);
+    if (e & 0x10000u) p[0] = static_cast<uint8_t>(cw);
+    if (e & 0x20000u) p[1] = static_cast<uint8_t>(cw >> 8);
+    if (e & 0x40000u) p[2] = static_cast<uint8_t>(cw >> 16);
+    if (e & 0x80000u) p[3] = static_cast<uint8_t>(cw >> 24);
     base += static_cast<int>((T >> sh) & 0xFFu);
   }
   return total;
@@ -273,7 +315,8 @@ struct alignas(128) DsSmem {
 
 __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     despace_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
-                   const int64_t *__restrict__ counts, int64_t tpc, int64_t *out_len) {
+                   const int64_t *__restrict__ counts, const uint32_t *__restrict__ masks,
+                   int64_t tpc, int64_t *out_len) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   DsSmem &S = *reinterpret_cast<DsSmem *>(smem_raw);
   const int tid = threadIdx.x;
@@ -283,25 +326,23 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     for (int s = 0; s < kCpStages; ++s) ptx::mbar_init(&S.cp.full[s], 1);
     ptx::fence_mbar_init();
   }
+  init_ktab(S.cp.ktab);
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tpc;
   const int64_t t1 = t0 + tpc < G.ntiles ? t0 + tpc : G.ntiles;
   int64_t running, total;
   chunk_prefix(counts, gridDim.x, blockIdx.x, running, total, S.red);  // has a __syncthreads
   const uint64_t pol = ptx::policy_evict_first();
   if (tid == 0)
-    for (int s = 0; s < kCpStages - 1 && t0 + s < t1; ++s) cp_load(S.cp, G, t0 + s, s, pol);
+    for (int s = 0; s < kCpStages - 1 && t0 + s < t1; ++s) cp_load(S.cp, G, masks, t0 + s, s, pol);
   const uintptr_t obase = reinterpret_cast<uintptr_t>(out);
   for (int64_t t = t0; t < t1; ++t) {
     const int it = static_cast<int>(t - t0);
     const int s = it % kCpStages;
     if (tid == 0 && t + kCpStages - 1 < t1)
-      cp_load(S.cp, G, t + kCpStages - 1, (it + kCpStages - 1) % kCpStages, pol);
+      cp_load(S.cp, G, masks, t + kCpStages - 1, (it + kCpStages - 1) % kCpStages, pol);
     ptx::mbar_wait_spin(&S.cp.full[s], static_cast<uint32_t>((it / kCpStages) & 1));
-    const int lo = G.lo(t), hi = G.hi(t);
     const int dst = static_cast<int>((obase + static_cast<uintptr_t>(running)) & 15);
-    const int n = (lo != 0 || hi != kCpTile)
-                      ? compact_tile<true>(S.cp.win[s], lo, hi, S.stream, dst, S.cp.wcnt)
-                      : compact_tile<false>(S.cp.win[s], lo, hi, S.stream, dst, S.cp.wcnt);
+    const int n = compact_tile(S.cp.win[s], S.cp.msk[s], S.stream, dst, S.cp.wcnt, S.cp.ktab);
     ptx::fence_proxy_async_smem();  // generic reads of win[s] before its next bulk write
     __syncthreads();
     cta_copy_out_congruent(out + running, S.stream + dst, n);

@@ -736,16 +736,23 @@ static void cp_plan(const void *d_in, int64_t m, int sms, int64_t *ntiles, int64
   *grid = (*ntiles + *tpc - 1) / *tpc;
 }
 
+// Keep masks: 4 bytes per thread slot per tile = 1/8 of the window bytes.
+static size_t cp_mask_bytes(int64_t m) {
+  const int64_t ntiles = (15 + m + kCpTile - 1) / kCpTile;
+  return 4 * kCpThreads * static_cast<size_t>(ntiles);
+}
+
 size_t b64_despace_workspace_bytes(int64_t m) {
   if (m < 0) return 0;
-  return 8 * kCpMaxChunks;  // per-chunk kept counts
+  return 8 * kCpMaxChunks + cp_mask_bytes(m);  // per-chunk kept counts + keep masks
 }
 
 int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_len, void *d_ws,
                 size_t ws_bytes, b64_stream_t stream) {
   if (m < 0 || d_out_len == nullptr || (m > 0 && (d_in == nullptr || d_out == nullptr)))
     return B64_ERR_ARG;
-  if (m > 0 && (d_ws == nullptr || ws_bytes < b64_despace_workspace_bytes(m)))
+  if (m > 0 && (d_ws == nullptr || ws_bytes < b64_despace_workspace_bytes(m) ||
+                 (reinterpret_cast<uintptr_t>(d_ws) & 15) != 0))
     return B64_ERR_WORKSPACE;
   if (m == 0)
     return cudaMemsetAsync(d_out_len, 0, sizeof(int64_t), stream) == cudaSuccess ? B64_OK
@@ -755,17 +762,18 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
   int64_t ntiles, tpc, grid;
   cp_plan(d_in, m, sms, &ntiles, &tpc, &grid);
   int64_t *counts = static_cast<int64_t *>(d_ws);
-  cp_count_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(d_in, m, tpc, counts,
-                                                                           nullptr);
+  uint32_t *masks = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(d_ws) + 8 * kCpMaxChunks);
+  cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(d_in, m, tpc, counts,
+                                                                          masks, nullptr);
   despace_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(DsSmem), stream>>>(
-      d_in, m, d_out, counts, tpc, d_out_len);
+      d_in, m, d_out, counts, masks, tpc, d_out_len);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
 size_t b64_decode_ws_workspace_bytes(int64_t m) {
   if (m < 0) return 0;
   const int64_t ntiles = (15 + m + kCpTile - 1) / kCpTile;
-  return kWsHdrBytes + 8 * kCpMaxChunks + 4 * static_cast<size_t>(ntiles);
+  return kWsHdrBytes + 8 * kCpMaxChunks + cp_mask_bytes(m) + 4 * static_cast<size_t>(ntiles);
 }
 
 int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
@@ -789,11 +797,12 @@ int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
   uint8_t *base = static_cast<uint8_t *>(d_ws);
   WsHdr *hdr = reinterpret_cast<WsHdr *>(base);
   int64_t *counts = reinterpret_cast<int64_t *>(base + kWsHdrBytes);
-  int32_t *tcnt = reinterpret_cast<int32_t *>(base + kWsHdrBytes + 8 * kCpMaxChunks);
-  cp_count_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(
-      d_in, m, tpc, counts, &hdr->errkey);
+  uint32_t *masks = reinterpret_cast<uint32_t *>(base + kWsHdrBytes + 8 * kCpMaxChunks);
+  int32_t *tcnt = reinterpret_cast<int32_t *>(base + kWsHdrBytes + 8 * kCpMaxChunks + cp_mask_bytes(m));
+  cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(
+      d_in, m, tpc, counts, masks, &hdr->errkey);
   decode_ws_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(WsSmem), stream>>>(
-      d_in, m, d_out, counts, tcnt, tpc, hdr, d_result, flags);
+      d_in, m, d_out, counts, masks, tcnt, tpc, hdr, d_result, flags);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 

@@ -3,7 +3,7 @@
 // followed by Algorithm 2 (with the f1/f2 flags) on the kept
 // characters, in one pass over the text after a counting pass:
 //
-//   cp_count_kernel  kept characters per chunk (b64_compact.cuh)
+//   cp_mask_kernel   keep masks per tile, kept characters per chunk (b64_compact.cuh)
 //   decode_ws_kernel per chunk: TMA-stage each 16 KiB tile, compact it into a
 //                    shared-memory stream (compact_tile), decode every 16-char
 //                    block of the compacted stream the chunk owns straight
@@ -152,7 +152,8 @@ __device__ int64_t ws_map_offset(WsSmem &S, const CpGeom &G, const int64_t *coun
 
 __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     decode_ws_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
-                     const int64_t *__restrict__ counts, int32_t *__restrict__ tcnt, int64_t tpc,
+                     const int64_t *__restrict__ counts, const uint32_t *__restrict__ masks,
+                     int32_t *__restrict__ tcnt, int64_t tpc,
                      WsHdr *hdr, b64_result *res, int flags) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   WsSmem &S = *reinterpret_cast<WsSmem *>(smem_raw);
@@ -160,6 +161,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
   CpGeom G;
   G.init(in, m, tpc);
   if (tid < 256) g_dec_tab[tid] = kInvalid;
+  init_ktab(S.cp.ktab);
   if (tid == 0) {
     for (int s = 0; s < kCpStages; ++s) ptx::mbar_init(&S.cp.full[s], 1);
     ptx::fence_mbar_init();
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
   const bool pads_ok = (M % 4) == 0;
   const uint64_t pol = ptx::policy_evict_first();
   if (tid == 0)
-    for (int s = 0; s < kCpStages - 1 && t0 + s < t1; ++s) cp_load(S.cp, G, t0 + s, s, pol);
+    for (int s = 0; s < kCpStages - 1 && t0 + s < t1; ++s) cp_load(S.cp, G, masks, t0 + s, s, pol);
 
   const int64_t own0 = (Pb + 15) & ~static_cast<int64_t>(15);  // first block this chunk owns
   int64_t Q = Pb, Bprev = Pb & ~static_cast<int64_t>(15);
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     const int it = static_cast<int>(t - t0);
     const int s = it % kCpStages, sb = it & 1;
     if (tid == 0 && t + kCpStages - 1 < t1)
-      cp_load(S.cp, G, t + kCpStages - 1, (it + kCpStages - 1) % kCpStages, pol);
+      cp_load(S.cp, G, masks, t + kCpStages - 1, (it + kCpStages - 1) % kCpStages, pol);
     const int64_t Bc = Q & ~static_cast<int64_t>(15);
     const int dst = static_cast<int>(Q & 15);
     // carry: the characters [Bc, Q) of an incomplete block, from the previous stream
@@ -191,10 +193,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
       *reinterpret_cast<uint4 *>(S.stream[sb]) =
           *reinterpret_cast<const uint4 *>(S.stream[sb ^ 1] + (Bc - Bprev));
     ptx::mbar_wait_spin(&S.cp.full[s], static_cast<uint32_t>((it / kCpStages) & 1));
-    const int lo = G.lo(t), hi = G.hi(t);
-    const int n = (lo != 0 || hi != kCpTile)
-                      ? compact_tile<true>(S.cp.win[s], lo, hi, S.stream[sb], dst, S.cp.wcnt)
-                      : compact_tile<false>(S.cp.win[s], lo, hi, S.stream[sb], dst, S.cp.wcnt);
+    const int n = compact_tile(S.cp.win[s], S.cp.msk[s], S.stream[sb], dst, S.cp.wcnt, S.cp.ktab);
     ptx::fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) tcnt[t] = n;
