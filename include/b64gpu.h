@@ -193,6 +193,20 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
 
 /* -------------------------------------------- MIME line handling (f4) */
 
+/* Line-wrapped encode (reading R-wrap): Algorithm 1
+ * with variant `flags` (URL, NOPAD), and an end-of-line sequence
+ * -- "\r\n" if crlf = 1, "\n" if crlf = 0 -- after every line_chars
+ * characters and after the final (shorter) line; empty input gives empty
+ * output.  line_chars: a multiple of 4 in [4, 16384] (76 = MIME, RFC 2045;
+ * 64 = PEM).  The paper's comparison mentions MIME-style line handling in
+ * the Linux codec.  d_out capacity:
+ * b64_encoded_len_wrapped(n, line_chars, crlf, flags).  Asynchronous on
+ * `stream`; returns the output length, or B64_ERR_ARG (nothing launched) /
+ * B64_ERR_CUDA. */
+int64_t b64_encoded_len_wrapped(int64_t n, int line_chars, int crlf, int flags);
+int64_t b64_encode_wrapped(const uint8_t *d_in, int64_t n, uint8_t *d_out, int line_chars,
+                           int crlf, int flags, b64_stream_t stream);
+
 /* Whitespace-tolerant decode (reading R-ws-decode): the
  * Appendix B filter ("white-space characters ... should be removed
  * prior to processing"; removed set ' ', '\n', '\r') followed

@@ -35,6 +35,7 @@ EXPORTS = (
     "b64_decode_ex_async", "b64_encode_batch_ex", "b64_decode_batch_ex",
     "b64_despace_workspace_bytes", "b64_despace",
     "b64_decode_ws_workspace_bytes", "b64_decode_ws", "b64_decode_ws_async",
+    "b64_encoded_len_wrapped", "b64_encode_wrapped",
 )
 
 _lib = None
@@ -90,6 +91,8 @@ def load_library():
         "b64_despace_workspace_bytes": (sz, [i64]),
         "b64_despace": (i32, [vp, i64, vp, vp, vp, sz, vp]),
         "b64_decode_ws_workspace_bytes": (sz, [i64]),
+        "b64_encoded_len_wrapped": (i64, [i64, i32, i32, i32]),
+        "b64_encode_wrapped": (i64, [vp, i64, vp, i32, i32, i32, vp]),
         "b64_decode_ws_async": (i32, [vp, i64, vp, i32, vp, vp, sz, vp]),
         "b64_decode_ws": (i32, [vp, i64, vp, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), vp, sz,
                                 vp]),
@@ -435,3 +438,32 @@ def b64_decode_ws_async(inp, out, result, flags: int = 0, ws=None, stream=None):
                                  ws.numel(), _stream(stream, inp.device))
     if rc < 0:
         raise B64Error(rc, "b64_decode_ws_async")
+
+
+def b64_encoded_len_wrapped(n: int, line_chars: int = 76, crlf: bool = True, flags: int = 0) -> int:
+    return load_library().b64_encoded_len_wrapped(n, line_chars, int(crlf), flags)
+
+
+def b64_encode_wrapped(inp, out=None, line_chars: int = 76, crlf: bool = True, flags: int = 0,
+                       stream=None):
+    """Line-wrapped encode (EOL after every ``line_chars`` chars and after the
+    final line).  Returns the output view (asynchronous)."""
+    import torch
+
+    _check_u8_cuda(inp, "inp")
+    lib = load_library()
+    n = inp.numel()
+    cap = lib.b64_encoded_len_wrapped(n, line_chars, int(crlf), flags)
+    if cap < 0:
+        raise B64Error(cap, "b64_encoded_len_wrapped")
+    if out is None:
+        out = torch.empty(max(cap, 1), dtype=torch.uint8, device=inp.device)
+    else:
+        _check_u8_cuda(out, "out")
+        if out.numel() < cap:
+            raise ValueError("out too small")
+    r = lib.b64_encode_wrapped(_ptr(inp), n, _ptr(out), line_chars, int(crlf), flags,
+                               _stream(stream, inp.device))
+    if r < 0:
+        raise B64Error(r, "b64_encode_wrapped")
+    return out[:r]

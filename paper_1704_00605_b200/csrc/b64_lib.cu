@@ -24,6 +24,7 @@
 #include "b64_batch.cuh"
 #include "b64_compact.cuh"
 #include "b64_ws.cuh"
+#include "b64_wrap.cuh"
 
 namespace b64 {
 
@@ -367,6 +368,8 @@ bool device_setup(int *dev_out, int *sms_out) {
     if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return false;
     if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return false;
     if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return false;
+    if (set_smem(encode_wrap_kernel<true>, sizeof(WrSmem)) != cudaSuccess) return false;
+    if (set_smem(encode_wrap_kernel<false>, sizeof(WrSmem)) != cudaSuccess) return false;
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return false;
     di.attrs_set = true;
   }
@@ -820,6 +823,49 @@ int b64_decode_ws(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int
   if (out_len) *out_len = r.out_len;
   if (err_pos) *err_pos = r.err_pos;
   return r.status;
+}
+
+static bool wrap_args_ok(int64_t n, int line_chars, int crlf, int flags) {
+  return n >= 0 && flags_ok(flags) && line_chars >= 4 && line_chars <= kWrMaxLine &&
+         line_chars % 4 == 0 && (crlf == 0 || crlf == 1);
+}
+
+int64_t b64_encoded_len_wrapped(int64_t n, int line_chars, int crlf, int flags) {
+  if (!wrap_args_ok(n, line_chars, crlf, flags)) return B64_ERR_ARG;
+  const int64_t m = enc_len(n, flags);
+  return m + (crlf ? 2 : 1) * ((m + line_chars - 1) / line_chars);
+}
+
+int64_t b64_encode_wrapped(const uint8_t *d_in, int64_t n, uint8_t *d_out, int line_chars,
+                           int crlf, int flags, b64_stream_t stream) {
+  if (!wrap_args_ok(n, line_chars, crlf, flags) || (n > 0 && (d_in == nullptr || d_out == nullptr)))
+    return B64_ERR_ARG;
+  if (n == 0) return 0;
+  int dev, sms;
+  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  WrGeom W;
+  W.n = n;
+  W.m = enc_len(n, flags);
+  W.ng = (n + 2) / 3;
+  W.L = line_chars;
+  W.e = crlf ? 2 : 1;
+  W.G = line_chars / 4;
+  W.nlines = (W.m + W.L - 1) / W.L;
+  W.total = W.m + W.e * W.nlines;
+  W.Lt = kWrIn / (3 * W.G);
+  W.inv = W.G > 1 ? static_cast<uint32_t>(((1ull << 32) + W.G - 1) / W.G) : 0u;
+  const int64_t ntiles = (W.nlines + W.Lt - 1) / W.Lt;
+  int64_t grid = static_cast<int64_t>(sms) * 2;
+  if (grid > ntiles) grid = ntiles;
+  const bool u16 = crlf && (reinterpret_cast<uintptr_t>(d_out) & 1) == 0;
+  if (u16)
+    encode_wrap_kernel<true><<<static_cast<unsigned>(grid), kWrThreads, sizeof(WrSmem), stream>>>(
+        d_in, d_out, W, ntiles, flags);
+  else
+    encode_wrap_kernel<false><<<static_cast<unsigned>(grid), kWrThreads, sizeof(WrSmem), stream>>>(
+        d_in, d_out, W, ntiles, flags);
+  if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
+  return W.total;
 }
 
 int b64_shard(int64_t total, int unit, int world, int rank, int64_t *begin, int64_t *end) {

@@ -1,0 +1,143 @@
+// b64_wrap.cuh -- line-wrapped (MIME / PEM style) encode on the GPU
+// (reading R-wrap in DESIGN.md §3): Algorithm 1
+// (with the f1 variant flags) whose output carries an end-of-line
+// sequence (LF or CR LF) after every `L` characters and after the final line.
+//
+// L is a multiple of 4, so a group (3 bytes -> 4 chars) never straddles a
+// line: group g lands at line g / G, column 4 (g mod G) (G = L/4), i.e. at
+// output offset (g / G)(L + e) + 4 (g mod G).  A tile is Lt whole lines
+// (Lt * 3G <= 12 KiB of input): the input window is TMA-staged (16-byte
+// granules, any alignment), each thread encodes one group per step (lanes
+// take consecutive groups, so the 2-byte / 1-byte stores of a warp hit
+// consecutive shared-memory words), the group's line comes from one
+// multiply-high by a precomputed reciprocal, and the tile's output -- staged
+// congruent to its destination mod 16 -- leaves with 16-byte stores.
+#pragma once
+#include <cstdint>
+
+#include "b64_codec.cuh"
+#include "b64_compact.cuh"
+#include "b64_ptx.cuh"
+
+namespace b64 {
+
+constexpr int kWrThreads = 512;
+constexpr int kWrIn = 12288;                 // max input bytes per tile
+constexpr int kWrStages = 3;
+constexpr int kWrOut = kWrIn / 3 * 4 + 2 * (kWrIn / 3) + 32;  // max output bytes per tile (+ slack)
+constexpr int kWrMaxLine = 16384;            // line_chars limit (one line fits a tile)
+
+struct WrGeom {
+  int64_t n;       // input bytes
+  int64_t m;       // encoded characters (Alg 1 + flags)
+  int64_t ng;      // groups = ceil(n / 3)
+  int64_t nlines;  // ceil(m / L)
+  int64_t total;   // output bytes = m + e * nlines
+  int L, e, G;     // line chars, EOL bytes, groups per line
+  int Lt;          // lines per tile
+  uint32_t inv;    // ceil(2^32 / G) (G > 1; G = 1 is special-cased)
+};
+
+struct alignas(128) WrSmem {
+  uint8_t in[kWrStages][kWrIn + 64];
+  uint8_t out[2][kWrOut];
+  uint64_t full[kWrStages];
+};
+
+template <bool U16>
+__global__ void __launch_bounds__(kWrThreads, 2)
+    encode_wrap_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, WrGeom W,
+                       int64_t ntiles, int flags) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  WrSmem &S = *reinterpret_cast<WrSmem *>(smem_raw);
+  const int tid = threadIdx.x;
+  if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid, flags));  // Table I / II
+  if (tid == 0) {
+    for (int s = 0; s < kWrStages; ++s) ptx::mbar_init(&S.full[s], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  const bool pad = !(flags & kFlagNoPad);
+  const int64_t tin = static_cast<int64_t>(W.Lt) * 3 * W.G;       // input bytes per tile
+  const int64_t tout = static_cast<int64_t>(W.Lt) * (W.L + W.e);  // output bytes per tile
+  const uint64_t pol = ptx::policy_evict_first();
+  auto load = [&](int64_t t, int s) {
+    const int64_t src = t * tin;
+    const int64_t len = W.n - src < tin ? W.n - src : tin;
+    const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src);
+    const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
+    const uintptr_t g1 = (g + static_cast<uintptr_t>(len) + 15) & ~static_cast<uintptr_t>(15);
+    ptx::mbar_arrive_expect_tx(&S.full[s], static_cast<uint32_t>(g1 - g0));
+    ptx::bulk_g2s(S.in[s], reinterpret_cast<const void *>(g0), static_cast<uint32_t>(g1 - g0),
+                  &S.full[s], pol);
+  };
+  const int64_t t0 = blockIdx.x;
+  if (tid == 0)
+    for (int k = 0; k < kWrStages - 1 && t0 + k * gridDim.x < ntiles; ++k)
+      load(t0 + k * gridDim.x, k);
+  const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(g_enc_tab));
+  const int S_line = W.L + W.e;
+  const int64_t glast = W.ng - 1;
+  const int rem = static_cast<int>(W.n % 3);  // bytes of the final group (0 = full)
+  int it = 0;
+  for (int64_t t = t0; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % kWrStages, so = it & 1;
+    if (tid == 0 && t + (kWrStages - 1) * static_cast<int64_t>(gridDim.x) < ntiles)
+      load(t + (kWrStages - 1) * static_cast<int64_t>(gridDim.x), (it + kWrStages - 1) % kWrStages);
+    const int64_t src = t * tin, dst = t * tout;
+    const int64_t g0 = src / 3;  // first group of the tile
+    const int64_t gend = (g0 + static_cast<int64_t>(W.Lt) * W.G) < W.ng
+                             ? g0 + static_cast<int64_t>(W.Lt) * W.G : W.ng;
+    const int ngrp = static_cast<int>(gend - g0);
+    const int64_t dend = gend == W.ng ? W.total : dst + tout;
+    const int olen = static_cast<int>(dend - dst);
+    const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src)) & 15);
+    const int omis = static_cast<int>((reinterpret_cast<uintptr_t>(out) + static_cast<uintptr_t>(dst)) & 15);
+    const uint32_t *win = reinterpret_cast<const uint32_t *>(S.in[s]);
+    uint8_t *ob = S.out[so] + omis;
+    ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kWrStages) & 1));
+    for (int g = tid; g < ngrp; g += kWrThreads) {
+      // Alg 1 main loop body: 3 bytes -> 24-bit big-endian value
+      const int a = imis + 3 * g;
+      const uint32_t x = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+      const bool fin = g0 + g == glast;
+      const int kb = fin && rem ? rem : 3;  // input bytes of this group
+      const uint32_t xm = kb == 3 ? x : x & (kb == 1 ? 0xFFu : 0xFFFFu);  // missing bytes = 0
+      uint32_t c = enc_group<true>(__byte_perm(xm, 0u, 0x4012), tb);
+      int nc = 4;  // characters emitted (Alg 1 tail)
+      if (kb != 3) {
+        if (pad) {
+          c = kb == 1 ? (c & 0x0000FFFFu) | 0x3D3D0000u : (c & 0x00FFFFFFu) | 0x3D000000u;
+        } else {
+          nc = kb + 1;
+        }
+      }
+      const uint32_t line = W.G == 1 ? static_cast<uint32_t>(g) : __umulhi(static_cast<uint32_t>(g), W.inv);
+      const int col = g - static_cast<int>(line) * W.G;
+      uint8_t *p = ob + static_cast<int>(line) * S_line + 4 * col;
+      if (U16 && nc == 4) {
+        reinterpret_cast<uint16_t *>(p)[0] = static_cast<uint16_t>(c);
+        reinterpret_cast<uint16_t *>(p)[1] = static_cast<uint16_t>(c >> 16);
+      } else {
+        p[0] = static_cast<uint8_t>(c);
+        p[1] = static_cast<uint8_t>(c >> 8);
+        if (nc > 2) p[2] = static_cast<uint8_t>(c >> 16);
+        if (nc > 3) p[3] = static_cast<uint8_t>(c >> 24);
+      }
+      if (col == W.G - 1 || fin) {  // end of a line: EOL after its last character
+        uint8_t *q = p + nc;
+        if (W.e == 2) {
+          q[0] = '\r';
+          q[1] = '\n';
+        } else {
+          q[0] = '\n';
+        }
+      }
+    }
+    ptx::fence_proxy_async_smem();  // generic reads of in[s] before its next bulk write
+    __syncthreads();
+    cta_copy_out_congruent(out + dst, ob, olen);
+  }
+}
+
+}  // namespace b64

@@ -81,3 +81,16 @@ def test_shard_config5_balance():
         sizes.append((e - b + 2) // 3)
     assert set(sizes) <= {1_431_655_765, 1_431_655_766}
     assert sum(sizes) == 11_453_246_123
+
+
+def test_wrapped_len_matches_oracle_and_rejects_bad_lines():
+    import oracle
+
+    for n in [0, 1, 2, 3, 56, 57, 58, 1000, 1 << 30]:
+        for L in (4, 64, 76, 16384):
+            for crlf in (0, 1):
+                for fl in (0, 2):
+                    assert b64.b64_encoded_len_wrapped(n, L, bool(crlf), fl) == \
+                        oracle._load().oracle_encoded_len_wrapped(n, L, crlf, fl)
+    for bad in (0, 3, 6, 77, 16388):
+        assert b64.b64_encoded_len_wrapped(10, bad, True, 0) == b64.B64_ERR_ARG
