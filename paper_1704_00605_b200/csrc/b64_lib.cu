@@ -368,8 +368,9 @@ bool device_setup(int *dev_out, int *sms_out) {
     if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return false;
     if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return false;
     if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return false;
-    if (set_smem(encode_wrap_kernel<true>, sizeof(WrSmem)) != cudaSuccess) return false;
-    if (set_smem(encode_wrap_kernel<false>, sizeof(WrSmem)) != cudaSuccess) return false;
+    if (set_smem(encode_wrap_kernel<2, true>, sizeof(WrSmem)) != cudaSuccess) return false;
+    if (set_smem(encode_wrap_kernel<2, false>, sizeof(WrSmem)) != cudaSuccess) return false;
+    if (set_smem(encode_wrap_kernel<1, false>, sizeof(WrSmem)) != cudaSuccess) return false;
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return false;
     di.attrs_set = true;
   }
@@ -858,12 +859,10 @@ int64_t b64_encode_wrapped(const uint8_t *d_in, int64_t n, uint8_t *d_out, int l
   int64_t grid = static_cast<int64_t>(sms) * 2;
   if (grid > ntiles) grid = ntiles;
   const bool u16 = crlf && (reinterpret_cast<uintptr_t>(d_out) & 1) == 0;
-  if (u16)
-    encode_wrap_kernel<true><<<static_cast<unsigned>(grid), kWrThreads, sizeof(WrSmem), stream>>>(
-        d_in, d_out, W, ntiles, flags);
-  else
-    encode_wrap_kernel<false><<<static_cast<unsigned>(grid), kWrThreads, sizeof(WrSmem), stream>>>(
-        d_in, d_out, W, ntiles, flags);
+  auto f = u16 ? encode_wrap_kernel<2, true> : crlf ? encode_wrap_kernel<2, false>
+                                                    : encode_wrap_kernel<1, false>;
+  f<<<static_cast<unsigned>(grid), kWrThreads, sizeof(WrSmem), stream>>>(d_in, d_out, W, ntiles,
+                                                                          flags);
   if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
   return W.total;
 }

@@ -44,7 +44,36 @@ struct alignas(128) WrSmem {
   uint64_t full[kWrStages];
 };
 
+// 4 characters at p (U16: p is even -> two 2-byte stores).
 template <bool U16>
+__device__ __forceinline__ void store4(uint8_t *p, uint32_t c) {
+  if (U16) {
+    reinterpret_cast<uint16_t *>(p)[0] = static_cast<uint16_t>(c);
+    reinterpret_cast<uint16_t *>(p)[1] = static_cast<uint16_t>(c >> 16);
+  } else {
+    p[0] = static_cast<uint8_t>(c);
+    p[1] = static_cast<uint8_t>(c >> 8);
+    p[2] = static_cast<uint8_t>(c >> 16);
+    p[3] = static_cast<uint8_t>(c >> 24);
+  }
+}
+template <bool U16, int E>
+__device__ __forceinline__ void store_eol(uint8_t *q) {
+  if (E == 2) {
+    if (U16) {
+      *reinterpret_cast<uint16_t *>(q) = 0x0A0Du;  // "\r\n"
+    } else {
+      q[0] = '\r';
+      q[1] = '\n';
+    }
+  } else {
+    q[0] = '\n';
+  }
+}
+
+// E: end-of-line bytes (1 = LF, 2 = CR LF), W.e == E.  U16: E == 2 and the
+// destination is even (every 4-char group lands on an even offset).
+template <int E, bool U16>
 __global__ void __launch_bounds__(kWrThreads, 2)
     encode_wrap_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, WrGeom W,
                        int64_t ntiles, int flags) {
@@ -76,7 +105,7 @@ __global__ void __launch_bounds__(kWrThreads, 2)
     for (int k = 0; k < kWrStages - 1 && t0 + k * gridDim.x < ntiles; ++k)
       load(t0 + k * gridDim.x, k);
   const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(g_enc_tab));
-  const int S_line = W.L + W.e;
+  const int S_line = W.L + E;
   const int64_t glast = W.ng - 1;
   const int rem = static_cast<int>(W.n % 3);  // bytes of the final group (0 = full)
   int it = 0;
@@ -96,41 +125,50 @@ __global__ void __launch_bounds__(kWrThreads, 2)
     const uint32_t *win = reinterpret_cast<const uint32_t *>(S.in[s]);
     uint8_t *ob = S.out[so] + omis;
     ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kWrStages) & 1));
-    for (int g = tid; g < ngrp; g += kWrThreads) {
-      // Alg 1 main loop body: 3 bytes -> 24-bit big-endian value
-      const int a = imis + 3 * g;
-      const uint32_t x = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
-      const bool fin = g0 + g == glast;
-      const int kb = fin && rem ? rem : 3;  // input bytes of this group
-      const uint32_t xm = kb == 3 ? x : x & (kb == 1 ? 0xFFu : 0xFFFFu);  // missing bytes = 0
-      uint32_t c = enc_group<true>(__byte_perm(xm, 0u, 0x4012), tb);
-      int nc = 4;  // characters emitted (Alg 1 tail)
-      if (kb != 3) {
-        if (pad) {
-          c = kb == 1 ? (c & 0x0000FFFFu) | 0x3D3D0000u : (c & 0x00FFFFFFu) | 0x3D000000u;
-        } else {
-          nc = kb + 1;
+    if (gend != W.ng) {
+      // Fast path: no tail group in this tile (Alg 1 main loop only).
+      const int ngl = ngrp;
+#pragma unroll 4
+      for (int g = tid; g < ngl; g += kWrThreads) {
+        const int a = imis + 3 * g;
+        const uint32_t x = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+        const uint32_t c = enc_group<true>(__byte_perm(x, 0u, 0x4012), tb);
+        const uint32_t line =
+            W.G == 1 ? static_cast<uint32_t>(g) : __umulhi(static_cast<uint32_t>(g), W.inv);
+        const int col = g - static_cast<int>(line) * W.G;
+        uint8_t *p = ob + static_cast<int>(line) * S_line + 4 * col;
+        store4<U16>(p, c);
+        if (col == W.G - 1) store_eol<U16, E>(p + 4);
+      }
+    } else {
+      for (int g = tid; g < ngrp; g += kWrThreads) {
+        const int a = imis + 3 * g;
+        const uint32_t x = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+        const bool fin = g0 + g == glast;
+        const int kb = fin && rem ? rem : 3;  // input bytes of this group
+        const uint32_t xm = kb == 3 ? x : x & (kb == 1 ? 0xFFu : 0xFFFFu);  // missing bytes = 0
+        uint32_t c = enc_group<true>(__byte_perm(xm, 0u, 0x4012), tb);
+        int nc = 4;  // characters emitted (Alg 1 tail)
+        if (kb != 3) {
+          if (pad) {
+            c = kb == 1 ? (c & 0x0000FFFFu) | 0x3D3D0000u : (c & 0x00FFFFFFu) | 0x3D000000u;
+          } else {
+            nc = kb + 1;
+          }
         }
-      }
-      const uint32_t line = W.G == 1 ? static_cast<uint32_t>(g) : __umulhi(static_cast<uint32_t>(g), W.inv);
-      const int col = g - static_cast<int>(line) * W.G;
-      uint8_t *p = ob + static_cast<int>(line) * S_line + 4 * col;
-      if (U16 && nc == 4) {
-        reinterpret_cast<uint16_t *>(p)[0] = static_cast<uint16_t>(c);
-        reinterpret_cast<uint16_t *>(p)[1] = static_cast<uint16_t>(c >> 16);
-      } else {
-        p[0] = static_cast<uint8_t>(c);
-        p[1] = static_cast<uint8_t>(c >> 8);
-        if (nc > 2) p[2] = static_cast<uint8_t>(c >> 16);
-        if (nc > 3) p[3] = static_cast<uint8_t>(c >> 24);
-      }
-      if (col == W.G - 1 || fin) {  // end of a line: EOL after its last character
-        uint8_t *q = p + nc;
-        if (W.e == 2) {
-          q[0] = '\r';
-          q[1] = '\n';
-        } else {
-          q[0] = '\n';
+        const uint32_t line =
+            W.G == 1 ? static_cast<uint32_t>(g) : __umulhi(static_cast<uint32_t>(g), W.inv);
+        const int col = g - static_cast<int>(line) * W.G;
+        uint8_t *p = ob + static_cast<int>(line) * S_line + 4 * col;
+        for (int k = 0; k < nc; ++k) p[k] = static_cast<uint8_t>(c >> (8 * k));
+        if (col == W.G - 1 || fin) {  // end of a line: EOL after its last character
+          uint8_t *q = p + nc;
+          if (W.e == 2) {
+            q[0] = '\r';
+            q[1] = '\n';
+          } else {
+            q[0] = '\n';
+          }
         }
       }
     }
