@@ -28,6 +28,19 @@ namespace b64 {
 
 using namespace ptx;
 
+#ifdef B64_BATCH_TRACE  // measurement only (tools/sweep.py): per-warp globaltimer stamps
+__device__ unsigned long long g_trace[148 * 64 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define B64_TRACE(slot) \
+  if (lane == 0) g_trace[(blockIdx.x * 64 + warp) * 4 + (slot)] = gtimer()
+#else
+#define B64_TRACE(slot)
+#endif
+
 constexpr int kBWarps = B64_BATCH_WARPS;
 constexpr int kBSlots = B64_BATCH_SLOTS;
 static_assert((kBSlots & (kBSlots - 1)) == 0, "batch ring depth must be a power of two");
@@ -242,7 +255,7 @@ __device__ __forceinline__ void warp_copy_out_congruent(uint8_t *gdst, const uin
     const int head = static_cast<int>(a0 - g);
     const int ng = static_cast<int>((a1 - a0) >> 4);
     for (int q = lane; q < ng; q += 32) {
-      const uint4 v = *reinterpret_cast<const uint4 *>(sbuf + head + 16 * q);
+      const uint4 v = lds128(sbuf + head + 16 * q);  // congruent: 16-byte aligned
       *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a0) + 16 * q) = v;
     }
     const int tail0 = static_cast<int>(a1 - g);
@@ -278,6 +291,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid, flags));
   }
   const bool pad = !(flags & kFlagNoPad);
+  B64_TRACE(0);
   if (lane == 0) {
     for (int s = 0; s < kBSlots; ++s) mbar_init(&R.full[s], 1);
     fence_mbar_init();
@@ -356,6 +370,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   __threadfence();
   grid.sync();
 
+  B64_TRACE(1);
 #ifdef B64_BATCH_PLAN_ONLY  // measurement only (tools/sweep.py): stop after the plan
   return;
 #endif
@@ -421,6 +436,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   for (int32_t it = 0; it < nu; ++it) {
     const int s = it & (kBSlots - 1);
     mbar_wait_spin(&R.full[s], static_cast<uint32_t>((it / kBSlots) & 1));
+    if (it == 0) B64_TRACE(2);
     const UnitDesc d = R.desc[s];
     const uintptr_t gsrc = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
     const int imis = static_cast<int>(gsrc & 15);
@@ -493,6 +509,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     __syncwarp();
   }
   }  // u_begin < u_end
+  B64_TRACE(3);
 
   if constexpr (DECODE) {
     // ---- phase 3: per-message results.  After the grid sync every error

@@ -297,7 +297,7 @@ __device__ __forceinline__ void cta_copy_out_congruent(uint8_t *dst, const uint8
     const int ng = static_cast<int>((a1 - a0) >> 4);
     for (int q = tid; q < ng; q += blockDim.x)
       *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a0) + 16 * q) =
-          *reinterpret_cast<const uint4 *>(src + head + 16 * q);
+          ptx::lds128(src + head + 16 * q);  // congruent: 16-byte aligned
     const int tail0 = static_cast<int>(a1 - g);
     if (tid < head) dst[tid] = src[tid];
     if (tid >= 32 && tid - 32 < n - tail0) dst[tail0 + tid - 32] = src[tail0 + tid - 32];

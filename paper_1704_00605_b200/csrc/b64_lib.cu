@@ -895,4 +895,10 @@ const char *b64_status_str(int status) {
 
 const char *b64_build_info(void) { return "libb64gpu sm_100a (tcgen-free byte codec; TMA bulk I/O)"; }
 
+#ifdef B64_BATCH_TRACE
+int b64_debug_trace(unsigned long long *host, int n) {
+  return cudaMemcpyFromSymbol(host, b64::g_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -2;
+}
+#endif
+
 }  // extern "C"

@@ -104,6 +104,17 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// 16-byte shared-memory load from an address the caller knows is 16-byte
+// aligned (forces LDS.128 where the compiler cannot prove the alignment).
+__device__ __forceinline__ uint4 lds128(const void *p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p))
+               : "memory");
+  return v;
+}
+
 // L2 eviction policies (createpolicy); streaming data is evict_first.
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

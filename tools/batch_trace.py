@@ -1,0 +1,50 @@
+#!/usr/bin/env python
+"""Per-warp timeline of the batched kernel (trace build, B64_BATCH_TRACE):
+runs one C2 batched encode and decode with the variant library named by
+B64GPU_LIB and prints the distribution of the globaltimer stamps (kernel
+start, plan done, first unit data ready, warp done) relative to the earliest."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1704_00605_b200 as b64  # noqa: E402
+from inputs import workloads as W  # noqa: E402
+from inputs.gpu_gen import fill  # noqa: E402
+
+lib = b64.load_library()
+dev = torch.device("cuda", 0)
+lens, _ = W.c2_lengths()
+off = W.offsets_from_lengths(lens)
+tot = int(off[-1])
+raw = torch.empty(tot, dtype=torch.uint8, device=dev)
+fill(raw, W.C2_SEED)
+doff = torch.from_numpy(off).to(dev)
+k = lens.size
+mt = int(sum(4 * ((int(L) + 2) // 3) for L in lens))
+out = torch.empty(mt + 16, dtype=torch.uint8, device=dev)
+out_off = torch.empty(k + 1, dtype=torch.int64, device=dev)
+wse = torch.empty(b64.b64_batch_workspace_bytes(k, tot, 0) + 256, dtype=torch.uint8, device=dev)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+N = 148 * 64 * 4
+buf = (ctypes.c_ulonglong * N)()
+lib.b64_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+for rep in range(4):
+    flush.zero_()
+    torch.cuda.synchronize()
+    b64.b64_encode_batch(raw, doff, out=out, out_off=out_off, ws=wse)
+    torch.cuda.synchronize()
+lib.b64_debug_trace(ctypes.addressof(buf), N)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64, 4).astype(np.int64)
+nw = int(os.environ.get("B64_TRACE_WARPS", "16"))
+a = a[:, :nw, :].reshape(-1, 4)
+t0 = a[:, 0].min()
+r = (a - t0) / 1000.0  # us
+for i, name in enumerate(["start", "plan_done", "first_data", "done"]):
+    v = r[:, i]
+    print(f"{name:10} min {v.min():7.2f} p10 {np.percentile(v,10):7.2f} p50 {np.median(v):7.2f} "
+          f"p90 {np.percentile(v,90):7.2f} max {v.max():7.2f} us")

@@ -52,6 +52,16 @@ VARIANTS = {
     "b_s8": {"B64_BATCH_SLOTS": 8, "B64_BATCH_WARPS": 8},
     "b_w8": {"B64_BATCH_WARPS": 8},
     "b_skel": {"B64_SKELETON": 1},
+    "b_p2_w32": {"B64_BATCH_PASSES": 2, "B64_BATCH_WARPS": 32},
+    "b_w24": {"B64_BATCH_WARPS": 24},
+    "b_p2_w24_s8": {"B64_BATCH_PASSES": 2, "B64_BATCH_WARPS": 24, "B64_BATCH_SLOTS": 8},
+    "b_p2_w16_s8": {"B64_BATCH_PASSES": 2, "B64_BATCH_WARPS": 16, "B64_BATCH_SLOTS": 8},
+    "b_p2_w32_skel": {"B64_BATCH_PASSES": 2, "B64_BATCH_WARPS": 32, "B64_SKELETON": 1},
+    "b_w20": {"B64_BATCH_WARPS": 20},
+    "b_trace": {"B64_BATCH_TRACE": 1},
+    "b_trace_skel": {"B64_BATCH_TRACE": 1, "B64_SKELETON": 1},
+    "b_w20_skel": {"B64_BATCH_WARPS": 20, "B64_SKELETON": 1},
+    "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
 }
 
 
