@@ -64,12 +64,9 @@ struct UnitDesc {
   int64_t src;     // input offset of the unit (relative to d_in)
   int64_t dst;     // output offset (relative to d_out)
   int64_t rel;     // input offset of the unit within its message
-  int64_t mlen;    // message length (input bytes)
-  int64_t mcap;    // message output reservation (out_off[i+1] - out_off[i])
   int32_t len;     // input bytes of the unit (decode: multiple of 4, > 0)
   int32_t msg;     // message index
   int32_t flags;   // kFlagLast | kFlagFinal
-  int32_t nunits;  // units of the message
 };
 
 template <int IN, int OUT>
@@ -78,7 +75,6 @@ struct alignas(16) WarpRing {
   static constexpr int kOutStride = round_up_c(OUT + 48, 16);  // 16 head room + 32 read slack
   uint8_t in[kBSlots][kInStride];
   uint8_t out[kOutStride];
-  UnitDesc desc[kBSlots];
   uint64_t full[kBSlots];
 };
 using EncRing = WarpRing<EU::kIn, EU::kOut>;
@@ -200,6 +196,55 @@ __device__ __forceinline__ int64_t find_message(const int64_t *unit_off, int64_t
   }
   return lo;
 }
+
+// A position in the unit sequence: the current message's metadata (pulled
+// from the lane-resident window with shuffles), advanced message by message.
+template <bool DECODE>
+struct Walker {
+  MsgWindow win;
+  int64_t msg, m_in, m_end, m_out, m_u0, m_u1;
+  __device__ __forceinline__ int64_t field(int64_t v, int64_t j) const {
+    return __shfl_sync(0xffffffffu, v, static_cast<int>(j - win.base));
+  }
+  __device__ __forceinline__ void pull() {
+    m_in = field(win.io, msg);
+    m_end = field(win.io, msg + 1);
+    m_out = field(win.oo, msg);
+    m_u0 = field(win.uo, msg);
+    m_u1 = field(win.uo, msg + 1);
+  }
+  __device__ __forceinline__ void init(int64_t m, int64_t k, const int64_t *in_off,
+                                       const int64_t *out_off, const int64_t *unit_off, int lane) {
+    msg = m;
+    window_load(win, m, k, in_off, out_off, unit_off, lane);
+    pull();
+  }
+  // Descriptor of unit u (u >= the current message's first unit).
+  __device__ __forceinline__ UnitDesc seek(int64_t u, int64_t k, const int64_t *in_off,
+                                           const int64_t *out_off, const int64_t *unit_off,
+                                           int lane) {
+    constexpr int UIN = DECODE ? DU::kIn : EU::kIn;
+    constexpr int UOUT = DECODE ? DU::kOut : EU::kOut;
+    while (u >= m_u1) {  // advance to the message holding unit u (skips empty messages)
+      ++msg;
+      if (msg + 1 >= win.base + 32) window_load(win, msg, k, in_off, out_off, unit_off, lane);
+      pull();
+    }
+    const int64_t r = u - m_u0;
+    const int64_t mlen = m_end - m_in;
+    const int64_t eff = DECODE ? (mlen & ~static_cast<int64_t>(3)) : mlen;
+    UnitDesc d;
+    d.rel = r * UIN;
+    d.src = m_in + d.rel;
+    d.dst = m_out + r * UOUT;
+    const int64_t left = eff - d.rel;
+    d.len = static_cast<int32_t>(left < UIN ? left : UIN);
+    d.msg = static_cast<int32_t>(msg);
+    const bool last = u == m_u1 - 1;
+    d.flags = (last ? kFlagLast : 0) | ((DECODE && last && (mlen & 3) == 0) ? kFlagFinal : 0);
+    return d;
+  }
+};
 
 // 16 stream bytes starting at byte offset `so` (any alignment) of a
 // 16-byte aligned smem stream: two conflict-free LDS.128 + a uniform
@@ -382,48 +427,22 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const int64_t u_end = static_cast<int64_t>((static_cast<__int128>(U) * (gw + 1)) / GW);
   if (u_begin < u_end) {
   const uint64_t pol = policy_evict_first();
-  // ---- issue-side walker state
-  MsgWindow win;
-  int64_t msg = find_message(unit_off, k, u_begin, lane);
-  window_load(win, msg, k, in_off, out_off, unit_off, lane);
-  auto field = [&](int64_t v, int64_t j) { return __shfl_sync(0xffffffffu, v, static_cast<int>(j - win.base)); };
-  int64_t m_in = field(win.io, msg), m_end = field(win.io, msg + 1);
-  int64_t m_out = field(win.oo, msg), m_oend = field(win.oo, msg + 1);
-  int64_t m_u0 = field(win.uo, msg), m_u1 = field(win.uo, msg + 1);
+  // Two walkers over the same unit sequence, both in registers: the issue
+  // walker runs kBSlots units ahead (TMA loads), the consume walker
+  // re-derives each unit's descriptor when its data has landed (no
+  // descriptor round trip through shared memory).
+  Walker<DECODE> wi, wc;
+  wi.init(find_message(unit_off, k, u_begin, lane), k, in_off, out_off, unit_off, lane);
+  wc = wi;
 
   auto issue = [&](int64_t u) {
-    while (u >= m_u1) {  // advance to the message holding unit u (skips empty messages)
-      ++msg;
-      if (msg + 1 >= win.base + 32) window_load(win, msg, k, in_off, out_off, unit_off, lane);
-      m_in = field(win.io, msg);
-      m_end = field(win.io, msg + 1);
-      m_out = field(win.oo, msg);
-      m_oend = field(win.oo, msg + 1);
-      m_u0 = field(win.uo, msg);
-      m_u1 = field(win.uo, msg + 1);
-    }
-    const int64_t r = u - m_u0;
-    const int64_t mlen = m_end - m_in;
-    const int64_t eff = DECODE ? 4 * (mlen / 4) : mlen;
-    UnitDesc d;
-    d.rel = r * UIN;
-    d.src = m_in + d.rel;
-    d.dst = m_out + r * UOUT;
-    const int64_t left = eff - d.rel;
-    d.len = static_cast<int32_t>(left < UIN ? left : UIN);
-    d.msg = static_cast<int32_t>(msg);
-    d.nunits = static_cast<int32_t>(m_u1 - m_u0);
-    d.mlen = mlen;
-    d.mcap = m_oend - m_out;
-    const bool last = u == m_u1 - 1;
-    d.flags = (last ? kFlagLast : 0) | ((DECODE && last && (mlen & 3) == 0) ? kFlagFinal : 0);
+    const UnitDesc d = wi.seek(u, k, in_off, out_off, unit_off, lane);
     if (lane == 0) {
       const int s = static_cast<int>(u - u_begin) & (kBSlots - 1);
-      R.desc[s] = d;
       const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
       const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
-      const uintptr_t g1 = (g + static_cast<uintptr_t>(d.len) + 15) & ~static_cast<uintptr_t>(15);
-      const uint32_t bytes = static_cast<uint32_t>(g1 - g0);
+      const uint32_t bytes =
+          (static_cast<uint32_t>(g & 15) + static_cast<uint32_t>(d.len) + 15u) & ~15u;
       mbar_arrive_expect_tx(&R.full[s], bytes);
       bulk_g2s(R.in[s], reinterpret_cast<const void *>(g0), bytes, &R.full[s], pol);
     }
@@ -435,9 +454,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const int32_t nu = static_cast<int32_t>(u_end - u_begin);
   for (int32_t it = 0; it < nu; ++it) {
     const int s = it & (kBSlots - 1);
+    const UnitDesc d = wc.seek(u_begin + it, k, in_off, out_off, unit_off, lane);
     mbar_wait_spin(&R.full[s], static_cast<uint32_t>((it / kBSlots) & 1));
     if (it == 0) B64_TRACE(2);
-    const UnitDesc d = R.desc[s];
     const uintptr_t gsrc = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
     const int imis = static_cast<int>(gsrc & 15);
     const bool in4 = (gsrc & 3) == 0;
@@ -464,7 +483,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
         encode_tile<1, 4, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane, nullptr,
                                                           pad);
       }
-      olen = static_cast<int>(enc_len(d.len, flags));
+      // enc_len of a unit (< 2^31 bytes): 32-bit arithmetic
+      olen = pad ? 4 * ((d.len + 2) / 3) : 4 * (d.len / 3) + (d.len % 3 ? d.len % 3 + 1 : 0);
     } else {
       const bool fin = (d.flags & kFlagFinal) != 0;
       uint32_t ch1 = 0, ch2 = 0;
