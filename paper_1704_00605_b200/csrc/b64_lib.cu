@@ -439,15 +439,15 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
 }
 
 // Batched workspace: [per-CTA totals (2 x 1024 int64) | unit_off[k+1] (int64)
-// | msg_done[k] (u32)].
+// | first_msg[kMaxBatchCtas * kBWarps] (i32)].
 constexpr int kMaxBatchCtas = 1024;
 size_t ws_layout(int64_t k, size_t *off_units, size_t *off_done) {
   size_t o = 2 * kMaxBatchCtas * sizeof(int64_t);
   *off_units = o;
   o += static_cast<size_t>(k + 1) * sizeof(int64_t);
   o = (o + 255) & ~static_cast<size_t>(255);
-  *off_done = o;
-  o += static_cast<size_t>(k > 0 ? k : 1) * sizeof(unsigned int);
+  *off_done = o;  // first_msg[grid * kBWarps] (int32): each warp's first message
+  o += static_cast<size_t>(kMaxBatchCtas) * kBWarps * sizeof(int32_t);
   return (o + 255) & ~static_cast<size_t>(255);
 }
 
@@ -572,7 +572,7 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
   uint8_t *ws = static_cast<uint8_t *>(d_ws);
   int64_t *blk = reinterpret_cast<int64_t *>(ws);
   int64_t *unit_off = reinterpret_cast<int64_t *>(ws + off_units);
-  unsigned int *done = reinterpret_cast<unsigned int *>(ws + off_done);
+  int32_t *done = reinterpret_cast<int32_t *>(ws + off_done);
   if (k == 0) {
     // nothing to plan: d_out_off[0] = 0
     const int64_t zero = 0;
@@ -589,7 +589,7 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
   int64_t *a_out_off = d_out_off, *a_unit = unit_off, *a_blk = blk;
   int64_t *a_err = d_err_pos, *a_len = d_out_len;
   int32_t *a_st = d_status;
-  unsigned int *a_done = done;
+  int32_t *a_done = done;
   int a_flags = flags;
   void *args[] = {&a_in, &a_out, &a_k, &a_in_off, &a_out_off, &a_unit, &a_blk,
                   &a_err, &a_len, &a_st, &a_done, &a_flags};

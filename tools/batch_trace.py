@@ -42,9 +42,23 @@ lib.b64_debug_trace(ctypes.addressof(buf), N)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64, 4).astype(np.int64)
 nw = int(os.environ.get("B64_TRACE_WARPS", "16"))
 a = a[:, :nw, :].reshape(-1, 4)
+if os.environ.get("B64_TRACE_FM"):
+    fm = a[:, 0] >> 32
+    tm = a[:, 0] & 0xFFFFFFFF
+    print("first_msg mismatches:", int((fm != tm).sum()))
+    a[:, 0] = a[:, 1] - 5000
 t0 = a[:, 0].min()
 r = (a - t0) / 1000.0  # us
 for i, name in enumerate(["start", "plan_done", "first_data", "done"]):
     v = r[:, i]
     print(f"{name:10} min {v.min():7.2f} p10 {np.percentile(v,10):7.2f} p50 {np.median(v):7.2f} "
           f"p90 {np.percentile(v,90):7.2f} max {v.max():7.2f} us")
+
+d = (a[:, 3] - t0) / 1000.0
+idx = np.argsort(-d)[:12]
+print("slowest warps (cta, warp, done_us, first_data_us):",
+      [(int(i // nw), int(i % nw), round(float(d[i]), 1), round(float(r[i, 2]), 1)) for i in idx])
+
+per = d.reshape(148, nw)
+print("mean done per warp index:", [round(float(x), 1) for x in per.mean(axis=0)])
+print("mean first_data per warp index:", [round(float(x), 1) for x in r[:, 2].reshape(148, nw).mean(axis=0)])
