@@ -2,18 +2,27 @@
 # Round-end evidence on the GPU box: plain runs first (must exit 0), then
 #  * ncu --set full of encode_kernel / decode_kernel on C3 (one launch each)
 #  * ncu --set full of the batched kernels on C2
+#  * ncu --set full of the f3/f4 kernels (despace, mime workloads)
 #  * DRAM bytes of the C5 launches (single-pass metrics, no replay of 80 GB)
 #  * the launch list (gpu__time_duration) of the default bench command
 set -u
 T=${1:-r01}
 mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { echo build failed; exit 1; }
+NCU="ncu --set full --clock-control none --import-source on"
 B3="python bench.py --workload c3 --steps 2 --warmup 3 --no-e2e --no-cpu"
 $B3 > gpurun_out/${T}_c3plain.json 2>&1 || { echo "c3 plain failed"; exit 1; }
-ncu --set full --clock-control none --import-source on -k regex:encode_kernel -s 3 -c 1 -o gpurun_out/${T}_enc_c3 -f $B3 > gpurun_out/${T}_ncu_enc.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 3 -c 1 -o gpurun_out/${T}_dec_c3 -f $B3 > gpurun_out/${T}_ncu_dec.log 2>&1
+$NCU -k regex:encode_kernel -s 3 -c 1 -o gpurun_out/${T}_enc_c3 -f $B3 > gpurun_out/${T}_ncu_enc.log 2>&1
+$NCU -k regex:decode_kernel -s 3 -c 1 -o gpurun_out/${T}_dec_c3 -f $B3 > gpurun_out/${T}_ncu_dec.log 2>&1
 B2="python bench.py --workload c2 --steps 1 --warmup 3"
 $B2 > gpurun_out/${T}_c2plain.json 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:batch_kernel -s 4 -c 2 -o gpurun_out/${T}_batch_c2 -f $B2 > gpurun_out/${T}_ncu_c2.log 2>&1
+$NCU -k regex:batch_kernel -s 4 -c 2 -o gpurun_out/${T}_batch_c2 -f $B2 > gpurun_out/${T}_ncu_c2.log 2>&1
+BD="python bench.py --workload despace --steps 1 --warmup 3"
+$BD > gpurun_out/${T}_dsplain.json 2>&1 && \
+$NCU -k regex:"cp_mask|despace" -s 4 -c 2 -o gpurun_out/${T}_despace -f $BD > gpurun_out/${T}_ncu_ds.log 2>&1
+BM="python bench.py --workload mime --steps 1 --warmup 3"
+$BM > gpurun_out/${T}_mimeplain.json 2>&1 && \
+$NCU -k regex:"encode_wrap|cp_mask|decode_ws" -s 6 -c 3 -o gpurun_out/${T}_mime -f $BM > gpurun_out/${T}_ncu_mime.log 2>&1
 B5="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu"
 $B5 > gpurun_out/${T}_c5plain.json 2>&1 && \
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
@@ -22,4 +31,7 @@ D="python bench.py"
 $D > gpurun_out/${T}_bench_plain.json 2> gpurun_out/${T}_bench_plain.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/${T}_launches.csv $D > gpurun_out/${T}_ncu_launch.log 2>&1
+for w in c1 c2 c4 despace mime; do
+  python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/${T}_bench_$w.json 2> gpurun_out/${T}_bench_$w.err
+done
 echo profile-all-done
