@@ -249,6 +249,18 @@ int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out
  * so only the last rank sees a partial unit.  Pure host. */
 int b64_shard(int64_t total, int unit, int world, int rank, int64_t *begin, int64_t *end);
 
+/* Batch sharding by message: rank `rank` of `world` gets
+ * the contiguous messages [*msg_begin, *msg_end) -- the batch's bytes
+ * h_in_off[0] .. h_in_off[k] cut into `world` equal-byte ranges, each cut
+ * moved to the next message boundary, so no message is split and every
+ * message belongs to exactly one rank (a rank may get none).  h_in_off:
+ * HOST int64[k+1], nondecreasing.  Each rank then runs the batched calls on
+ * its slice (offsets rebased to its first message); per-message results
+ * are gathered (paper_1704_00605_b200.dist).  Pure host; B64_ERR_ARG on bad
+ * arguments. */
+int b64_batch_shard(const int64_t *h_in_off, int64_t k, int world, int rank, int64_t *msg_begin,
+                    int64_t *msg_end);
+
 /* Static string for a status code. */
 const char *b64_status_str(int status);
 

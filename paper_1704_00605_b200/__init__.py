@@ -21,6 +21,7 @@ from ._lib import (  # noqa: F401
     b64_decode_ex,
     b64_despace,
     b64_decode_ws,
+    b64_batch_shard,
     b64_encode_wrapped,
     b64_encoded_len_wrapped,
     b64_decode_ws_async,

@@ -30,7 +30,7 @@ EXPORTS = (
     "b64_encoded_len", "b64_decoded_max_len", "b64_encode", "b64_decode",
     "b64_decode_async", "b64_decode_shard_async", "b64_batch_workspace_bytes",
     "b64_encode_batch", "b64_decode_batch", "b64_encode_host", "b64_decode_host",
-    "b64_shard", "b64_status_str", "b64_build_info",
+    "b64_shard", "b64_batch_shard", "b64_status_str", "b64_build_info",
     "b64_encoded_len_ex", "b64_decoded_max_len_ex", "b64_encode_ex", "b64_decode_ex",
     "b64_decode_ex_async", "b64_encode_batch_ex", "b64_decode_batch_ex",
     "b64_despace_workspace_bytes", "b64_despace",
@@ -79,6 +79,7 @@ def load_library():
         "b64_encode_host": (i64, [vp, i64, vp, vp, vp, vp]),
         "b64_decode_host": (i32, [vp, i64, vp, p64, p64, vp, vp, vp]),
         "b64_shard": (i32, [i64, i32, i32, i32, p64, p64]),
+        "b64_batch_shard": (i32, [vp, i64, i32, i32, p64, p64]),
         "b64_status_str": (ctypes.c_char_p, [i32]),
         "b64_build_info": (ctypes.c_char_p, []),
         "b64_encoded_len_ex": (i64, [i64, i32]),
@@ -354,6 +355,21 @@ def b64_shard(total: int, unit: int, world: int, rank: int) -> tuple[int, int]:
     rc = load_library().b64_shard(total, unit, world, rank, ctypes.byref(b), ctypes.byref(e))
     if rc < 0:
         raise B64Error(rc, "b64_shard")
+    return b.value, e.value
+
+
+def b64_batch_shard(in_off, world: int, rank: int) -> tuple[int, int]:
+    """Messages [begin, end) of rank's equal-byte share of a batch (C ABI
+    b64_batch_shard); ``in_off`` is a host int64 array of k+1 offsets."""
+    import numpy as np
+
+    off = np.ascontiguousarray(np.asarray(in_off, dtype=np.int64))
+    b = ctypes.c_int64(0)
+    e = ctypes.c_int64(0)
+    rc = load_library().b64_batch_shard(off.ctypes.data, off.size - 1, world, rank, ctypes.byref(b),
+                                        ctypes.byref(e))
+    if rc < 0:
+        raise B64Error(rc, "b64_batch_shard")
     return b.value, e.value
 
 

@@ -880,6 +880,32 @@ int b64_shard(int64_t total, int unit, int world, int rank, int64_t *begin, int6
   return B64_OK;
 }
 
+int b64_batch_shard(const int64_t *h_in_off, int64_t k, int world, int rank, int64_t *msg_begin,
+                    int64_t *msg_end) {
+  if (h_in_off == nullptr || k < 0 || world <= 0 || rank < 0 || rank >= world || !msg_begin ||
+      !msg_end)
+    return B64_ERR_ARG;
+  const int64_t base = h_in_off[0];
+  const __int128 T = static_cast<__int128>(h_in_off[k]) - base;
+  if (T < 0) return B64_ERR_ARG;
+  // first message whose start is at or beyond byte floor(T*r/G) of the batch
+  auto boundary = [&](int r) -> int64_t {
+    if (r == 0) return 0;
+    if (r == world) return k;
+    const int64_t target = base + static_cast<int64_t>(T * r / world);
+    int64_t lo = 0, hi = k;  // smallest i in [0, k] with h_in_off[i] >= target
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (h_in_off[mid] >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    return lo;
+  };
+  *msg_begin = boundary(rank);
+  *msg_end = boundary(rank + 1);
+  return B64_OK;
+}
+
 const char *b64_status_str(int status) {
   switch (status) {
     case B64_OK: return "ok";
