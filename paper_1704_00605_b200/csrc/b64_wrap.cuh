@@ -108,6 +108,11 @@ __global__ void __launch_bounds__(kWrThreads, 2)
   const int S_line = W.L + E;
   const int64_t glast = W.ng - 1;
   const int rem = static_cast<int>(W.n % 3);  // bytes of the final group (0 = full)
+  // thread-invariant walk of the fast path: group tid + 512 k
+  const int line_t = tid / W.G, col_t = tid % W.G;
+  const int p_t = line_t * S_line + 4 * col_t;
+  const int dc = kWrThreads % W.G;
+  const int pstep = (kWrThreads / W.G) * S_line + 4 * dc;
   int it = 0;
   for (int64_t t = t0; t < ntiles; t += gridDim.x, ++it) {
     const int s = it % kWrStages, so = it & 1;
@@ -123,22 +128,32 @@ __global__ void __launch_bounds__(kWrThreads, 2)
     const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src)) & 15);
     const int omis = static_cast<int>((reinterpret_cast<uintptr_t>(out) + static_cast<uintptr_t>(dst)) & 15);
     const uint32_t *win = reinterpret_cast<const uint32_t *>(S.in[s]);
+    const int a_t = imis + 3 * tid;
+    const uint32_t sh_t = 8u * static_cast<uint32_t>(a_t & 3);
     uint8_t *ob = S.out[so] + omis;
     ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kWrStages) & 1));
     if (gend != W.ng) {
-      // Fast path: no tail group in this tile (Alg 1 main loop only).
-      const int ngl = ngrp;
+      // Fast path: a full tile (Lt whole lines, no tail group).  Every tile
+      // starts on a line boundary and the stride 512 is a multiple of 4
+      // bytes of input, so a thread's input word offset / byte shift and its
+      // (line, column) walk are tile-invariant: no per-group division or
+      // address arithmetic beyond one increment.
+      const uint32_t *wp = win + (a_t >> 2);
+      uint8_t *p = ob + p_t;
+      int col = col_t;
 #pragma unroll 4
-      for (int g = tid; g < ngl; g += kWrThreads) {
-        const int a = imis + 3 * g;
-        const uint32_t x = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+      for (int g = tid; g < ngrp; g += kWrThreads) {
+        const uint32_t x = __funnelshift_r(wp[0], wp[1], sh_t);
         const uint32_t c = enc_group<true>(__byte_perm(x, 0u, 0x4012), tb);
-        const uint32_t line =
-            W.G == 1 ? static_cast<uint32_t>(g) : __umulhi(static_cast<uint32_t>(g), W.inv);
-        const int col = g - static_cast<int>(line) * W.G;
-        uint8_t *p = ob + static_cast<int>(line) * S_line + 4 * col;
         store4<U16>(p, c);
         if (col == W.G - 1) store_eol<U16, E>(p + 4);
+        wp += 3 * kWrThreads / 4;
+        p += pstep;
+        col += dc;
+        if (col >= W.G) {
+          col -= W.G;
+          p += E;
+        }
       }
     } else {
       for (int g = tid; g < ngrp; g += kWrThreads) {
