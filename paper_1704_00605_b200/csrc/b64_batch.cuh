@@ -499,26 +499,24 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const bool in4 = (gsrc & 3) == 0;
     const uint8_t *sin = R.in[s] + imis;
     uint8_t *gdst = out + d.dst;
-    // Encode outputs start on 4-byte boundaries (out_off are sums of 4*ceil(len/3)):
-    // stage congruent to the destination (aligned word stores, aligned copy).
-    // Decode outputs start anywhere: stage aligned and realign on copy-out.
-    const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
-    const bool congruent = !DECODE && (omis & 3) == 0;
-    uint8_t *sout = congruent ? R.out + 16 + omis : R.out + 16;
+    // Output is staged 16-byte aligned (whole-lane STS.128 for full encode
+    // passes, no bank conflicts) and realigned per 16-byte granule on the
+    // copy-out (two LDS.128 + funnel shift per STG.128).  (Staging encode
+    // output congruent to the destination turned every pass into four
+    // 4-way-conflicted STS.32 for the 3/4 of units whose destination is not
+    // 16-byte aligned.)
+    uint8_t *sout = R.out + 16;
     int olen;
     uint32_t werr = 0xFFFFFFFFu;
     if constexpr (!DECODE) {
-      if (!congruent) {  // destination not 4-byte aligned: aligned stream + realigning copy
+      if (d.len == UIN) {
+        if (in4)
+          encode_tile<4, 16, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+        else
+          encode_tile<1, 16, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
+      } else {
         encode_tile<1, 16, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane, nullptr,
                                                            pad);
-      } else if (d.len == UIN) {
-        if (in4)
-          encode_tile<4, 4, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
-        else
-          encode_tile<1, 4, true, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane);
-      } else {
-        encode_tile<1, 4, false, kBatchPasses, false, 32>(sin, d.len, sout, lane, lane, nullptr,
-                                                          pad);
       }
       // enc_len of a unit (< 2^31 bytes): 32-bit arithmetic
       olen = pad ? 4 * ((d.len + 2) / 3) : 4 * (d.len / 3) + (d.len % 3 ? d.len % 3 + 1 : 0);
@@ -550,10 +548,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       issue(iu);
       ++iu;
     }
-    if (congruent)
-      warp_copy_out_congruent(gdst, sout, olen, lane);
-    else
-      warp_copy_out(gdst, sout, olen, lane);
+    warp_copy_out(gdst, sout, olen, lane);
     if constexpr (DECODE) {
       // First-error reduction: the warp's minimum offset of the
       // unit, one 64-bit atomicMin on the message's slot (error path only).
