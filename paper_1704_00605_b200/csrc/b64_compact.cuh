@@ -39,7 +39,10 @@ constexpr int kCpWarpWords = kCpWords / kCpWarps;   // 256 words = 1 KiB per war
 constexpr int kCpPerLane = kCpWarpWords / 32;       // 8 words per lane
 static_assert(kCpPerLane == 8, "compact_tile packs 8 keep nibbles per lane");
 constexpr int kCpStages = 3;                        // TMA input ring depth
-constexpr int kCpCtasPerSm = 2;
+#ifndef B64_CP_CTAS
+#define B64_CP_CTAS 2
+#endif
+constexpr int kCpCtasPerSm = B64_CP_CTAS;
 constexpr int kCpMaxChunks = 4096;
 
 // Per-byte keep flags: bit 7 of each byte of the result is set iff that byte

@@ -59,6 +59,7 @@ VARIANTS = {
     "b_p2_w32_skel": {"B64_BATCH_PASSES": 2, "B64_BATCH_WARPS": 32, "B64_SKELETON": 1},
     "b_w20": {"B64_BATCH_WARPS": 20},
     "b_trace": {"B64_BATCH_TRACE": 1},
+    "cp3": {"B64_CP_CTAS": 3},
     "b_trace_fm": {"B64_BATCH_TRACE": 1, "B64_BATCH_TRACE_FM": 1},
     "b_trace_sw": {"B64_BATCH_TRACE": 1, "B64_BATCH_SYNCWARP": 1},
     "b_trace_sw0": {"B64_BATCH_TRACE": 1, "B64_BATCH_SYNCWARP0": 1},
