@@ -379,11 +379,19 @@ def run_small_configs(args):
     K, Wm = args.steps, args.warmup
     res = b64.result_tensor(dev)
 
-    def timed(fn):
-        tot = 0.0
+    samples = {}
+    clocks = ClockSampler(dev.index or 0)
+
+    def timed(fn, name=None, flush_l2=True):
+        ts = []
         for k in range(Wm + K):
-            flush.zero_()
-            flush_rd.amax()
+            if flush_l2:
+                flush.zero_()
+                flush_rd.amax()
+            else:
+                # keep the GPU busy while the host enqueues the timed call, so
+                # the events bracket device time, not host submission latency
+                torch.cuda._sleep(200_000)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -391,11 +399,14 @@ def run_small_configs(args):
             e1.record(stream)
             torch.cuda.synchronize(dev)
             if k >= Wm:
-                tot += e0.elapsed_time(e1)
-        return tot / K  # ms per step
+                ts.append(e0.elapsed_time(e1))
+        if name:
+            samples[name] = {"min_ms": min(ts), "median_ms": statistics.median(ts)}
+        return sum(ts) / K  # ms per step (mean)
 
     wl = args.workload
     detail = {}
+    clocks.start()
     if wl == "c1":
         n = W.C1_N
         x = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -407,10 +418,13 @@ def run_small_configs(args):
         pos, byte = W.c1_corruption(m)
         td = t.clone()
         td[pos] = byte
-        enc_ms = timed(lambda: b64.b64_encode(x, out=t))
-        dec_ms = timed(lambda: b64.b64_decode_async(t, y, res))
-        dirty_ms = timed(lambda: b64.b64_decode_async(td, y, res))
+        enc_ms = timed(lambda: b64.b64_encode(x, out=t), "encode")
+        dec_ms = timed(lambda: b64.b64_decode_async(t, y, res), "decode")
+        dirty_ms = timed(lambda: b64.b64_decode_async(td, y, res), "dirty_decode")
         assert b64.unpack_result(res)[1] == pos
+        hot_enc = timed(lambda: b64.b64_encode(x, out=t), "encode_hot_l2", flush_l2=False)
+        hot_dec = timed(lambda: b64.b64_decode_async(t, y, res), "decode_hot_l2", flush_l2=False)
+        assert b64.unpack_result(res)[2] == 0
         # end-to-end sync API latency (includes the result read-back)
         t0 = time.perf_counter()
         for _ in range(200):
@@ -420,6 +434,7 @@ def run_small_configs(args):
         value = (n + 2 * m) / (ms / 1e3) / 1e9
         algo = {"encode": n + m, "decode": m + n}
         detail = {"encode_us": enc_ms * 1e3, "decode_us": dec_ms * 1e3, "dirty_decode_us": dirty_ms * 1e3,
+                  "encode_hot_l2_us": hot_enc * 1e3, "decode_hot_l2_us": hot_dec * 1e3,
                   "sync_decode_api_us": sync_us}
         dom, dom_ms = ("encode", enc_ms) if enc_ms >= dec_ms else ("decode", dec_ms)
         desc = "C1: 2^20 random bytes (seed 0): encode, decode, decode of a copy with one NA191 byte"
@@ -451,8 +466,8 @@ def run_small_configs(args):
             b64.b64_decode_batch(out, out_off, out=y, out_off=y_off, out_len=y_len, err_pos=y_err,
                                  status=y_st, ws=wsd, total_in=mt)
 
-        enc_ms = timed(enc)
-        dec_ms = timed(dec)
+        enc_ms = timed(enc, "encode")
+        dec_ms = timed(dec, "decode")
         if os.environ.get("B64_BENCH_NOCHECK") != "1":
             assert int(y_st.abs().sum().item()) == 0 and torch.equal(y[:tot], raw)
         ms = enc_ms + dec_ms
@@ -485,7 +500,7 @@ def run_small_configs(args):
         def ds():
             olen_t[0] = b64.b64_despace(w, out=out, ws=ws)[1]
 
-        ds_ms = timed(ds)
+        ds_ms = timed(ds, "despace")
         kept = int(olen_t[0].item())
         assert kept == t.numel() and torch.equal(out[:kept], t)
         ms = ds_ms
@@ -507,8 +522,8 @@ def run_small_configs(args):
         w = torch.empty(m, dtype=torch.uint8, device=dev)
         y = torch.empty(b64.b64_decoded_max_len(m), dtype=torch.uint8, device=dev)
         ws = torch.empty(b64.b64_decode_ws_workspace_bytes(m), dtype=torch.uint8, device=dev)
-        enc_ms = timed(lambda: b64.b64_encode_wrapped(raw, out=w, line_chars=76, crlf=True))
-        dec_ms = timed(lambda: b64.b64_decode_ws_async(w, y, res, ws=ws))
+        enc_ms = timed(lambda: b64.b64_encode_wrapped(raw, out=w, line_chars=76, crlf=True), "encode_wrapped")
+        dec_ms = timed(lambda: b64.b64_decode_ws_async(w, y, res, ws=ws), "decode_ws")
         ol, ep, st, _ = b64.unpack_result(res)
         assert (ol, ep, st) == (nraw, -1, 0) and torch.equal(y[:nraw], raw)
         assert int(w[76].item()) == 13 and int(w[77].item()) == 10
@@ -525,6 +540,38 @@ def run_small_configs(args):
         desc = ("f4: MIME round trip, 57*2^24 random bytes (seed 2) <-> 1.31 GB of 76-char CRLF lines: "
                 "line-wrapped encode + whitespace-tolerant decode")
         launches = 3
+    elif wl == "sweep":
+        # Fig. 9-shaped curve: GB/s vs input length, random
+        # bytes of seed 6, n in {2^k, 4 <= k <= 30} and the Table V file
+        # sizes.  Device time per call (CUDA events, mean of K
+        # calls after W warm-ups); L2 is not flushed (small sizes are
+        # latency-bound and L2-resident, as the paper's cache-hot loops).
+        sizes = sorted({1 << e for e in range(4, 31)} | {1355, 1484, 2357, 12640, 141020, 329632})
+        nmax = sizes[-1]
+        raw = torch.empty(nmax, dtype=torch.uint8, device=dev)
+        fill(raw, 6)
+        t = torch.empty(b64.b64_encoded_len(nmax), dtype=torch.uint8, device=dev)
+        y = torch.empty(nmax + 3, dtype=torch.uint8, device=dev)
+        curve = []
+        for n in sizes:
+            xv = raw[:n]
+            m = b64.b64_encoded_len(n)
+            tv = t[:m]
+            e_ms = timed(lambda: b64.b64_encode(xv, out=tv), flush_l2=False)
+            d_ms = timed(lambda: b64.b64_decode_async(tv, y, res), flush_l2=False)
+            assert b64.unpack_result(res)[2] == 0
+            curve.append({"n": n, "encode_us": e_ms * 1e3, "decode_us": d_ms * 1e3,
+                          "encode_GBps_input": n / (e_ms / 1e3) / 1e9,
+                          "decode_GBps_input": m / (d_ms / 1e3) / 1e9})
+        last = curve[-1]
+        ms = last["encode_us"] / 1e3 + last["decode_us"] / 1e3
+        value = (nmax + b64.b64_encoded_len(nmax)) / (ms / 1e3) / 1e9
+        algo = {"encode": nmax + b64.b64_encoded_len(nmax), "decode": b64.b64_encoded_len(nmax) + nmax}
+        dom, dom_ms = ("decode", last["decode_us"] / 1e3) if last["decode_us"] >= last["encode_us"] \
+            else ("encode", last["encode_us"] / 1e3)
+        detail = {"sweep": curve, "value_is": "encode + decode input GB/s at the largest size"}
+        desc = "sweep: encode/decode GB/s vs length (2^4 .. 2^30 and Table V sizes), seed 6, L2 not flushed"
+        launches = 2
     else:  # c4
         raw = torch.empty(W.C4_RAW, dtype=torch.uint8, device=dev)
         fill(raw, W.C4_SEED)
@@ -535,9 +582,9 @@ def run_small_configs(args):
         td = t.clone()
         td[torch.from_numpy(pos).to(dev)] = torch.from_numpy(byt).to(dev)
         y = torch.empty(b64.b64_decoded_max_len(m), dtype=torch.uint8, device=dev)
-        clean_ms = timed(lambda: b64.b64_decode_async(t, y, res))
+        clean_ms = timed(lambda: b64.b64_decode_async(t, y, res), "clean")
         assert b64.unpack_result(res)[2] == 0
-        dirty_ms = timed(lambda: b64.b64_decode_async(td, y, res))
+        dirty_ms = timed(lambda: b64.b64_decode_async(td, y, res), "dirty")
         assert b64.unpack_result(res)[1] == int(pos.min())
         ms = clean_ms + dirty_ms
         value = 2 * m / (ms / 1e3) / 1e9
@@ -547,6 +594,7 @@ def run_small_configs(args):
         dom, dom_ms = "decode", clean_ms
         desc = "C4: 256 MiB valid text (seed 3) decoded clean and with 256 NA191 bytes (seed 4)"
         launches = 2
+    clk = clocks.stop()
     ach = algo[dom] / (dom_ms / 1e3) / 1e9
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": K, "warmup": Wm,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
@@ -554,7 +602,9 @@ def run_small_configs(args):
             "config": {"workload": desc, "l2": "flushed before every step: 512 MiB write, then a 256 MiB read (drains the flush's dirty lines)"},
             "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel", "achieved": ach, "peak": hbm, "unit": "GB/s",
                          "frac": ach / hbm, "traffic": None, "peak_source": hbm_src},
-            "gpu_launches": launches * K, "detail": detail}
+            "gpu_launches": launches * K, "clocks": clk, "timing": samples, "detail": detail}
+    if wl == "sweep":
+        line["config"]["l2"] = "not flushed (cache-hot sweep)"
     print(json.dumps(line), flush=True)
 
 
@@ -603,7 +653,7 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c5", "c3", "c1", "c2", "c4", "despace", "mime"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c3", "c1", "c2", "c4", "despace", "mime", "sweep"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-bytes", type=int, default=3 << 28)
@@ -615,7 +665,7 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload in ("c1", "c2", "c4", "despace", "mime"):
+    elif args.workload in ("c1", "c2", "c4", "despace", "mime", "sweep"):
         run_small_configs(args)
     else:
         run_ours(args)

@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       res->pad_count = R.pad_count;
       ws->errkey = ~0ull;
       ws->done = 0;
-      __threadfence_system();
+      // (no system-scope fence: kernel completion makes these writes --
+      // device or mapped host memory -- visible to the synchronizing host)
     }
   }
 }

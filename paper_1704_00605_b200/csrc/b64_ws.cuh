@@ -318,7 +318,6 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     res->err_pos = oep;
     res->status = st;
     res->pad_count = pc;
-    __threadfence_system();
   }
 }
 
