@@ -137,8 +137,9 @@ __device__ __forceinline__ uint32_t tile_nib(const uint32_t (&w)[kCpPerLane], in
 __global__ void __launch_bounds__(kCpThreads)
     cp_mask_kernel(const uint8_t *__restrict__ in, int64_t m, int64_t tpc,
                    int64_t *__restrict__ counts, uint32_t *__restrict__ masks,
-                   unsigned long long *reset) {
+                   unsigned long long *reset, const int32_t *skip = nullptr) {
   __shared__ int64_t sh[66];
+  if (skip != nullptr && *skip == 1) return;  // the line-structured fast path already decoded
   if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     reset[0] = ~0ull;
     reset[1] = 0ull;

@@ -25,6 +25,7 @@
 #include "b64_compact.cuh"
 #include "b64_ws.cuh"
 #include "b64_wrap.cuh"
+#include "b64_wslines.cuh"
 
 namespace b64 {
 
@@ -369,6 +370,7 @@ bool device_setup(int *dev_out, int *sms_out) {
     if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return false;
     if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return false;
     if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return false;
+    if (set_smem(decode_lines_kernel, sizeof(WlSmem)) != cudaSuccess) return false;
     if (set_smem(encode_wrap_kernel<2, true>, sizeof(WrSmem)) != cudaSuccess) return false;
     if (set_smem(encode_wrap_kernel<2, false>, sizeof(WrSmem)) != cudaSuccess) return false;
     if (set_smem(encode_wrap_kernel<1, false>, sizeof(WrSmem)) != cudaSuccess) return false;
@@ -804,10 +806,16 @@ int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
   int64_t *counts = reinterpret_cast<int64_t *>(base + kWsHdrBytes);
   uint32_t *masks = reinterpret_cast<uint32_t *>(base + kWsHdrBytes + 8 * kCpMaxChunks);
   int32_t *tcnt = reinterpret_cast<int32_t *>(base + kWsHdrBytes + 8 * kCpMaxChunks + cp_mask_bytes(m));
+  // 1. verified fast path for line-structured text (MIME / PEM); 2-3. the
+  // general path, which returns at once when 1. succeeded.
+  WlState *wl = reinterpret_cast<WlState *>(base + kWlStateOffset);
+  if (cudaMemsetAsync(wl, 0, sizeof(WlState), stream) != cudaSuccess) return B64_ERR_CUDA;
+  decode_lines_kernel<<<static_cast<unsigned>(sms) * 2, kWlThreads, sizeof(WlSmem), stream>>>(
+      d_in, m, d_out, wl, d_result, flags);
   cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(
-      d_in, m, tpc, counts, masks, &hdr->errkey);
+      d_in, m, tpc, counts, masks, &hdr->errkey, &wl->verdict);
   decode_ws_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(WsSmem), stream>>>(
-      d_in, m, d_out, counts, masks, tcnt, tpc, hdr, d_result, flags);
+      d_in, m, d_out, counts, masks, tcnt, tpc, hdr, d_result, flags, &wl->verdict);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 

@@ -40,7 +40,8 @@ struct WsHdr {
   uint8_t tail[8];            // the final quad of the compacted stream
 };
 constexpr size_t kWsHdrBytes = 64;
-static_assert(sizeof(WsHdr) <= kWsHdrBytes, "WsHdr");
+constexpr size_t kWlStateOffset = 48;  // WlState (b64_wslines.cuh) lives in the header's tail
+static_assert(sizeof(WsHdr) <= kWlStateOffset, "WsHdr");
 
 struct alignas(128) WsSmem {
   CpSmem cp;
@@ -154,7 +155,8 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     decode_ws_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
                      const int64_t *__restrict__ counts, const uint32_t *__restrict__ masks,
                      int32_t *__restrict__ tcnt, int64_t tpc,
-                     WsHdr *hdr, b64_result *res, int flags) {
+                     WsHdr *hdr, b64_result *res, int flags, const int32_t *skip = nullptr) {
+  if (skip != nullptr && *skip == 1) return;  // the line-structured fast path already decoded
   extern __shared__ __align__(128) uint8_t smem_raw[];
   WsSmem &S = *reinterpret_cast<WsSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

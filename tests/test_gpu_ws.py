@@ -10,7 +10,7 @@ import torch
 import oracle
 import paper_1704_00605_b200 as b64
 from inputs.gen import splitmix_bytes
-from tests.gpu_util import empty_dev, host, to_dev
+from tests.gpu_util import DEV, empty_dev, host, to_dev
 
 pytestmark = pytest.mark.gpu
 TILE = 16384
@@ -157,3 +157,40 @@ def test_async_result_record():
     rst, rep, rout = oracle.decode_ws(w)
     assert (st, ep, ol) == (rst, rep, rout.size)
     assert np.array_equal(host(out[:ol]), rout)
+
+
+def _verdict(w, fl=0):
+    """Run the ws decode with an explicit workspace and return the fast-path
+    verdict stored in it (1 = line-structured fast path, 0 = general path)."""
+    ws = torch.empty(b64.b64_decode_ws_workspace_bytes(w.size) + 64, dtype=torch.uint8, device=DEV)
+    b64.b64_decode_ws(to_dev(w), flags=fl, ws=ws)
+    return int(ws[48:52].view(torch.int32).item())
+
+
+def test_fast_path_taken_exactly_on_line_structure():
+    x = splitmix_bytes(420, 0, 100_000)
+    assert _verdict(oracle.encode_wrapped(x, 76, crlf=True)) == 1
+    assert _verdict(oracle.encode_wrapped(x, 64, crlf=False)) == 1
+    assert _verdict(oracle.encode_wrapped(x[:1000], 76, crlf=True)[:-2]) == 1   # no final EOL
+    assert _verdict(oracle.encode_wrapped(x, 76, crlf=True, flags=NP), NP) == 1
+    assert _verdict(oracle.encode(x)) == 0                                   # no white space
+    w = oracle.encode_wrapped(x, 76, crlf=True)
+    for cut in (5, 78 * 500 + 77, w.size - 1):                               # a stray byte
+        u = np.insert(w, cut, ord(" "))
+        assert _verdict(u) == 0
+        check(u)
+    u = w.copy()
+    u[78 * 700 + 10] = ord("!")                                              # an error
+    assert _verdict(u) == 0
+    check(u)
+
+
+@pytest.mark.parametrize("L", [4, 8, 60, 64, 76, 1000, 4092])
+@pytest.mark.parametrize("crlf", [False, True])
+def test_line_structured_lengths(L, crlf):
+    # the fast path across tile seams for every line length; tails of 1..L chars
+    x = splitmix_bytes(421 + L, 0, 300_000)
+    for n in [1, 2, 3, 3 * L // 4, 3 * L // 4 + 1, 7 * L, 300_000]:
+        w = oracle.encode_wrapped(x[:n], L, crlf=crlf)
+        check(w)
+        check(w[: w.size - (2 if crlf else 1)])  # without the final EOL
