@@ -27,8 +27,14 @@
 namespace b64 {
 
 constexpr int kWlThreads = 512;
-constexpr int kWlTile = 16384;        // max input bytes per tile (whole lines)
-constexpr int kWlStages = 3;
+#ifndef B64_WL_TILE
+#define B64_WL_TILE 28672
+#endif
+#ifndef B64_WL_STAGES
+#define B64_WL_STAGES 2
+#endif
+constexpr int kWlTile = B64_WL_TILE;    // max input bytes per tile (whole lines)
+constexpr int kWlStages = B64_WL_STAGES;
 constexpr int kWlMaxLine = 4092;      // longest line the fast path takes
 constexpr int kWlOut = kWlTile / 4 * 3 + 64;
 

@@ -60,6 +60,10 @@ VARIANTS = {
     "b_w20": {"B64_BATCH_WARPS": 20},
     "b_trace": {"B64_BATCH_TRACE": 1},
     "cp3": {"B64_CP_CTAS": 3},
+    "wl16_3": {"B64_WL_TILE": 16384, "B64_WL_STAGES": 3},
+    "wl28_2": {"B64_WL_TILE": 28672, "B64_WL_STAGES": 2},
+    "wl24_2": {"B64_WL_TILE": 24576, "B64_WL_STAGES": 2},
+    "wl20_3": {"B64_WL_TILE": 20480, "B64_WL_STAGES": 3},
     "b_trace_fm": {"B64_BATCH_TRACE": 1, "B64_BATCH_TRACE_FM": 1},
     "b_trace_sw": {"B64_BATCH_TRACE": 1, "B64_BATCH_SYNCWARP": 1},
     "b_trace_sw0": {"B64_BATCH_TRACE": 1, "B64_BATCH_SYNCWARP0": 1},
