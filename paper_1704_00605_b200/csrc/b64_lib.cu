@@ -863,6 +863,7 @@ int64_t b64_encode_wrapped(const uint8_t *d_in, int64_t n, uint8_t *d_out, int l
   W.nlines = (W.m + W.L - 1) / W.L;
   W.total = W.m + W.e * W.nlines;
   W.Lt = kWrIn / (3 * W.G);
+  if (W.Lt > B64_WR_OUT / (W.L + W.e)) W.Lt = B64_WR_OUT / (W.L + W.e);
   W.inv = W.G > 1 ? static_cast<uint32_t>(((1ull << 32) + W.G - 1) / W.G) : 0u;
   const int64_t ntiles = (W.nlines + W.Lt - 1) / W.Lt;
   int64_t grid = static_cast<int64_t>(sms) * 2;

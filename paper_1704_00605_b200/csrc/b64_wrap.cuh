@@ -6,7 +6,7 @@
 // L is a multiple of 4, so a group (3 bytes -> 4 chars) never straddles a
 // line: group g lands at line g / G, column 4 (g mod G) (G = L/4), i.e. at
 // output offset (g / G)(L + e) + 4 (g mod G).  A tile is Lt whole lines
-// (Lt * 3G <= 12 KiB of input): the input window is TMA-staged (16-byte
+// (Lt * 3G <= kWrIn input bytes and Lt (L + e) <= B64_WR_OUT output bytes): the input window is TMA-staged (16-byte
 // granules, any alignment), each thread encodes one group per step (lanes
 // take consecutive groups, so the 2-byte / 1-byte stores of a warp hit
 // consecutive shared-memory words), the group's line comes from one
@@ -22,9 +22,18 @@
 namespace b64 {
 
 constexpr int kWrThreads = 512;
-constexpr int kWrIn = 12288;                 // max input bytes per tile
-constexpr int kWrStages = 3;
-constexpr int kWrOut = kWrIn / 3 * 4 + 2 * (kWrIn / 3) + 32;  // max output bytes per tile (+ slack)
+#ifndef B64_WR_IN
+#define B64_WR_IN 21504
+#endif
+#ifndef B64_WR_OUT
+#define B64_WR_OUT 28672
+#endif
+#ifndef B64_WR_STAGES
+#define B64_WR_STAGES 2
+#endif
+constexpr int kWrIn = B64_WR_IN;             // max input bytes per tile
+constexpr int kWrStages = B64_WR_STAGES;
+constexpr int kWrOut = B64_WR_OUT + 32;      // max output bytes per tile (+ staging slack)
 constexpr int kWrMaxLine = 16384;            // line_chars limit (one line fits a tile)
 
 struct WrGeom {

@@ -61,6 +61,10 @@ VARIANTS = {
     "b_trace": {"B64_BATCH_TRACE": 1},
     "cp3": {"B64_CP_CTAS": 3},
     "wl16_3": {"B64_WL_TILE": 16384, "B64_WL_STAGES": 3},
+    "wr12_3": {"B64_WR_IN": 12288, "B64_WR_OUT": 24576, "B64_WR_STAGES": 3},
+    "wr21_2": {"B64_WR_IN": 21504, "B64_WR_OUT": 28672, "B64_WR_STAGES": 2},
+    "wr18_2": {"B64_WR_IN": 18432, "B64_WR_OUT": 28672, "B64_WR_STAGES": 2},
+    "wr16_3": {"B64_WR_IN": 16384, "B64_WR_OUT": 22528, "B64_WR_STAGES": 3},
     "wl28_2": {"B64_WL_TILE": 28672, "B64_WL_STAGES": 2},
     "wl24_2": {"B64_WL_TILE": 24576, "B64_WL_STAGES": 2},
     "wl20_3": {"B64_WL_TILE": 20480, "B64_WL_STAGES": 3},
