@@ -31,9 +31,12 @@
 
 namespace b64 {
 
-constexpr int kCpWarps = 16;
+#ifndef B64_CP_WARPS
+#define B64_CP_WARPS 16
+#endif
+constexpr int kCpWarps = B64_CP_WARPS;  // warps per CTA; a tile is 1 KiB per warp
 constexpr int kCpThreads = kCpWarps * 32;
-constexpr int kCpTile = 16384;                      // input window bytes per tile
+constexpr int kCpTile = kCpWarps * 1024;            // input window bytes per tile
 constexpr int kCpWords = kCpTile / 4;               // 4096 words
 constexpr int kCpWarpWords = kCpWords / kCpWarps;   // 256 words = 1 KiB per warp
 constexpr int kCpPerLane = kCpWarpWords / 32;       // 8 words per lane
