@@ -314,9 +314,19 @@ __device__ __forceinline__ void cta_copy_out_congruent(uint8_t *dst, const uint8
 }
 
 // ------------------------------------------------------ despace (f3) ---
+#ifndef B64_DS_GROUP
+#define B64_DS_GROUP 1
+#endif
+constexpr int kDsGroup = B64_DS_GROUP;  // tiles compacted per copy-out
+constexpr int kDsStages = kCpStages + kDsGroup - 1;
+
 struct alignas(128) DsSmem {
-  CpSmem cp;
-  uint8_t stream[kCpTile + 32];
+  uint8_t win[kDsStages][kCpTile];
+  uint32_t msk[kDsStages][kCpThreads];
+  uint64_t full[kDsStages];
+  int32_t wcnt[2][kCpWarps];
+  uint32_t ktab[16];
+  alignas(16) uint8_t stream[kDsGroup * kCpTile + 32];  // 16-aligned: LDS.128 copy-out
   int64_t red[66];
 };
 
@@ -330,27 +340,45 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
   CpGeom G;
   G.init(in, m, tpc);
   if (tid == 0) {
-    for (int s = 0; s < kCpStages; ++s) ptx::mbar_init(&S.cp.full[s], 1);
+    for (int s = 0; s < kDsStages; ++s) ptx::mbar_init(&S.full[s], 1);
     ptx::fence_mbar_init();
   }
-  init_ktab(S.cp.ktab);
+  init_ktab(S.ktab);
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tpc;
   const int64_t t1 = t0 + tpc < G.ntiles ? t0 + tpc : G.ntiles;
   int64_t running, total;
   chunk_prefix(counts, gridDim.x, blockIdx.x, running, total, S.red);  // has a __syncthreads
   const uint64_t pol = ptx::policy_evict_first();
+  // TMA ring of kDsStages tiles (window + masks on one mbarrier each)
+  auto load = [&](int64_t t, int s) {
+    const int h = G.hi(t);
+    const uint32_t bytes = static_cast<uint32_t>((h + 15) & ~15);
+    ptx::mbar_arrive_expect_tx(&S.full[s], bytes + 4 * kCpThreads);
+    ptx::bulk_g2s(S.win[s], reinterpret_cast<const void *>(G.a0 + static_cast<uintptr_t>(t) * kCpTile),
+                  bytes, &S.full[s], pol);
+    ptx::bulk_g2s(S.msk[s], masks + t * kCpThreads, 4 * kCpThreads, &S.full[s], pol);
+  };
   if (tid == 0)
-    for (int s = 0; s < kCpStages - 1 && t0 + s < t1; ++s) cp_load(S.cp, G, masks, t0 + s, s, pol);
+    for (int s = 0; s < kDsStages - 1 && t0 + s < t1; ++s) load(t0 + s, s);
   const uintptr_t obase = reinterpret_cast<uintptr_t>(out);
-  for (int64_t t = t0; t < t1; ++t) {
-    const int it = static_cast<int>(t - t0);
-    const int s = it % kCpStages;
-    if (tid == 0 && t + kCpStages - 1 < t1)
-      cp_load(S.cp, G, masks, t + kCpStages - 1, (it + kCpStages - 1) % kCpStages, pol);
-    ptx::mbar_wait_spin(&S.cp.full[s], static_cast<uint32_t>((it / kCpStages) & 1));
+  int64_t t = t0;
+  while (t < t1) {
+    // kDsGroup tiles compacted back to back into one stream, one copy-out:
+    // a tile's input slot is refilled only after the next compact_tile's
+    // internal barrier (every warp is done reading it by then).
     const int dst = static_cast<int>((obase + static_cast<uintptr_t>(running)) & 15);
-    const int n = compact_tile(S.cp.win[s], S.cp.msk[s], S.stream, dst, S.cp.wcnt, S.cp.ktab);
-    ptx::fence_proxy_async_smem();  // generic reads of win[s] before its next bulk write
+    int n = 0;
+#pragma unroll 1
+    for (int j = 0; j < kDsGroup && t < t1; ++j, ++t) {
+      const int it = static_cast<int>(t - t0);
+      const int s = it % kDsStages;
+      ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kDsStages) & 1));
+      n += compact_tile(S.win[s], S.msk[s], S.stream, dst + n, S.wcnt[j & 1], S.ktab);
+      ptx::fence_proxy_async_smem();  // generic reads of win[s] before its next bulk write
+      // slot of tile t-1 is free (all warps passed this tile's internal barrier)
+      if (tid == 0 && t + kDsStages - 1 < t1)
+        load(t + kDsStages - 1, static_cast<int>((it + kDsStages - 1) % kDsStages));
+    }
     __syncthreads();
     cta_copy_out_congruent(out + running, S.stream + dst, n);
     running += n;

@@ -49,7 +49,7 @@ struct WrGeom {
 
 struct alignas(128) WrSmem {
   uint8_t in[kWrStages][kWrIn + 64];
-  uint8_t out[2][kWrOut];
+  alignas(16) uint8_t out[2][kWrOut];
   uint64_t full[kWrStages];
 };
 

@@ -45,8 +45,8 @@ static_assert(sizeof(WsHdr) <= kWlStateOffset, "WsHdr");
 
 struct alignas(128) WsSmem {
   CpSmem cp;
-  uint8_t stream[2][kCpTile + 64];  // compacted characters; [0] = compact position Bc (16-aligned)
-  uint8_t ostage[kCpTile / 4 * 3 + 64];
+  alignas(16) uint8_t stream[2][kCpTile + 64];  // compacted characters; [0] = compact position Bc (16-aligned)
+  alignas(16) uint8_t ostage[kCpTile / 4 * 3 + 64];
   alignas(16) uint8_t blk[64];                 // boundary block characters
   alignas(16) uint8_t bout[64];                 // boundary block output
   int64_t red[66];

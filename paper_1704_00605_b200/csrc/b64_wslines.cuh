@@ -49,7 +49,7 @@ struct WlState {
 
 struct alignas(128) WlSmem {
   uint8_t in[kWlStages][kWlTile + 64];
-  uint8_t out[2][kWlOut];
+  alignas(16) uint8_t out[2][kWlOut];
   uint64_t full[kWlStages];
   int64_t geo[4];   // Mc (kept chars), nlines, ok
   int32_t Le[2];    // L, e

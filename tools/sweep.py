@@ -60,6 +60,8 @@ VARIANTS = {
     "b_w20": {"B64_BATCH_WARPS": 20},
     "b_trace": {"B64_BATCH_TRACE": 1},
     "cp3": {"B64_CP_CTAS": 3},
+    "ds_g1": {"B64_DS_GROUP": 1},
+    "ds_g2": {"B64_DS_GROUP": 2},
     "cp_w32_c1": {"B64_CP_WARPS": 32, "B64_CP_CTAS": 1},
     "cp_w24_c1": {"B64_CP_WARPS": 24, "B64_CP_CTAS": 1},
     "wl16_3": {"B64_WL_TILE": 16384, "B64_WL_STAGES": 3},
