@@ -43,7 +43,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 constexpr int kBWarps = B64_BATCH_WARPS;
 constexpr int kBSlots = B64_BATCH_SLOTS;
-static_assert((kBSlots & (kBSlots - 1)) == 0, "batch ring depth must be a power of two");
 constexpr int kBThreads = kBWarps * 32;
 constexpr int kFlagLast = 2;  // unit is the last unit of its message
 
@@ -475,7 +474,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   auto issue = [&](int64_t u) {
     const UnitDesc d = wi.seek(u, k, in_off, out_off, unit_off, lane);
     if (lane == 0) {
-      const int s = static_cast<int>(u - u_begin) & (kBSlots - 1);
+      const int s = static_cast<int>((u - u_begin) % kBSlots);
       const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
       const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
       const uint32_t bytes =
@@ -490,7 +489,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
 
   const int32_t nu = static_cast<int32_t>(u_end - u_begin);
   for (int32_t it = 0; it < nu; ++it) {
-    const int s = it & (kBSlots - 1);
+    const int s = it % kBSlots;
     const UnitDesc d = wc.seek(u_begin + it, k, in_off, out_off, unit_off, lane);
     mbar_wait_spin(&R.full[s], static_cast<uint32_t>((it / kBSlots) & 1));
     if (it == 0) B64_TRACE(2);
