@@ -22,7 +22,10 @@ $BD > gpurun_out/${T}_dsplain.json 2>&1 && \
 $NCU -k regex:"cp_mask|despace" -s 4 -c 2 -o gpurun_out/${T}_despace -f $BD > gpurun_out/${T}_ncu_ds.log 2>&1
 BM="python bench.py --workload mime --steps 1 --warmup 3"
 $BM > gpurun_out/${T}_mimeplain.json 2>&1 && \
-$NCU -k regex:"encode_wrap|cp_mask|decode_ws" -s 6 -c 3 -o gpurun_out/${T}_mime -f $BM > gpurun_out/${T}_ncu_mime.log 2>&1
+$NCU -k regex:"encode_wrap|decode_lines" -s 6 -c 2 -o gpurun_out/${T}_mime -f $BM > gpurun_out/${T}_ncu_mime.log 2>&1
+BI="python bench.py --workload mime_irregular --steps 1 --warmup 3"
+$BI > gpurun_out/${T}_mimeirrplain.json 2>&1 && \
+$NCU -k regex:"cp_mask|decode_ws" -s 6 -c 2 -o gpurun_out/${T}_mimeirr -f $BI > gpurun_out/${T}_ncu_mimeirr.log 2>&1
 B5="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu"
 $B5 > gpurun_out/${T}_c5plain.json 2>&1 && \
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
@@ -31,7 +34,7 @@ D="python bench.py"
 $D > gpurun_out/${T}_bench_plain.json 2> gpurun_out/${T}_bench_plain.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/${T}_launches.csv $D > gpurun_out/${T}_ncu_launch.log 2>&1
-for w in c1 c2 c4 despace mime; do
+for w in c1 c2 c4 despace mime mime_irregular sweep; do
   python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/${T}_bench_$w.json 2> gpurun_out/${T}_bench_$w.err
 done
 echo profile-all-done
