@@ -2,14 +2,14 @@
 // (BASELINE.json configs[1]).
 //
 // Work is split into *units*: one unit = kBatchPasses passes of one warp
-// (encode: 768 input bytes -> 1024 chars; decode: 1024 chars -> 768 bytes).
+// (encode: 1536 input bytes -> 2048 chars; decode: 2048 chars -> 1536 bytes).
 // A unit never straddles messages, so a message of len bytes has
 // ceil(len / unit) units (at most one partial unit per message, <= 2-4 %
 // slack at data-URI sizes).  The planner scans the message lengths once
 // (output offsets + unit offsets); every warp of the persistent grid then
 // takes an equal, contiguous range of units -- i.e. messages are assigned to
-// warps by prefix-summed lengths -- finds its first message with one 32-ary
-// search and walks forward.  Warps are fully independent: each owns a
+// warps by prefix-summed lengths -- gets its first message from a table the
+// plan writes and walks forward.  Warps are fully independent: each owns a
 // 4-slot ring of 1-D TMA bulk loads (its lane 0 issues them, one mbarrier per
 // slot), a private output slice in smem, and writes its unit's output with
 // coalesced 16-byte stores (byte stores for the <16-byte unaligned edges).
@@ -300,29 +300,6 @@ __device__ __forceinline__ void warp_copy_out(uint8_t *gdst, const uint8_t *stre
   const int tail0 = head + body;
   if (lane < head) gdst[lane] = stream[lane];
   if (lane >= 16 && tail0 + lane - 16 < len) gdst[tail0 + lane - 16] = stream[tail0 + lane - 16];
-}
-
-// Congruent copy-out: `len` bytes staged at sbuf, which has the same address
-// mod 16 as gdst: interior granules by aligned LDS.128 / STG.128, the
-// unaligned edges byte-wise.
-__device__ __forceinline__ void warp_copy_out_congruent(uint8_t *gdst, const uint8_t *sbuf, int len,
-                                                        int lane) {
-  const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
-  const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
-  const uintptr_t a1 = (g + static_cast<uintptr_t>(len)) & ~static_cast<uintptr_t>(15);
-  if (a1 > a0) {
-    const int head = static_cast<int>(a0 - g);
-    const int ng = static_cast<int>((a1 - a0) >> 4);
-    for (int q = lane; q < ng; q += 32) {
-      const uint4 v = lds128(sbuf + head + 16 * q);  // congruent: 16-byte aligned
-      *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a0) + 16 * q) = v;
-    }
-    const int tail0 = static_cast<int>(a1 - g);
-    if (lane < head) gdst[lane] = sbuf[lane];
-    if (lane >= 16 && lane - 16 < len - tail0) gdst[tail0 + lane - 16] = sbuf[tail0 + lane - 16];
-  } else {
-    if (lane < len) gdst[lane] = sbuf[lane];
-  }
 }
 
 // --------------------------------------------------------- the kernel ---
