@@ -465,11 +465,17 @@ __global__ void __launch_bounds__(kBThreads, 1)
   for (; iu < u_end && iu < u_begin + kBSlots; ++iu) issue(iu);
 
   const int32_t nu = static_cast<int32_t>(u_end - u_begin);
+#ifdef B64_BATCH_TRACE
+  unsigned long long tr_bytes = 0;
+#endif
   for (int32_t it = 0; it < nu; ++it) {
     const int s = it % kBSlots;
     const UnitDesc d = wc.seek(u_begin + it, k, in_off, out_off, unit_off, lane);
     mbar_wait_spin(&R.full[s], static_cast<uint32_t>((it / kBSlots) & 1));
     if (it == 0) B64_TRACE(2);
+#ifdef B64_BATCH_TRACE
+    tr_bytes += static_cast<unsigned long long>(d.len);
+#endif
     const uintptr_t gsrc = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(d.src);
     const int imis = static_cast<int>(gsrc & 15);
     const bool in4 = (gsrc & 3) == 0;
@@ -536,6 +542,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
     }
     __syncwarp();
   }
+#ifdef B64_BATCH_TRACE
+  if (lane == 0)
+    g_trace[(blockIdx.x * 64 + warp) * 4 + 0] =
+        (tr_bytes << 20) | static_cast<unsigned long long>(u_end - u_begin);
+#endif
   }  // u_begin < u_end
   B64_TRACE(3);
 

@@ -42,7 +42,19 @@ lib.b64_debug_trace(ctypes.addressof(buf), N)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64, 4).astype(np.int64)
 nw = int(os.environ.get("B64_TRACE_WARPS", "16"))
 a = a[:, :nw, :].reshape(-1, 4)
-if os.environ.get("B64_TRACE_FM"):
+if os.environ.get("B64_TRACE_WORK"):
+    wb = a[:, 0] >> 20
+    wu = a[:, 0] & 0xFFFFF
+    d3 = (a[:, 3] - a[:, 1]) / 1000.0
+    print("units per warp: min", wu.min(), "max", wu.max(), " bytes per warp: min", wb.min(), "max", wb.max())
+    import numpy as _np
+    print("corr(done-plan, bytes) =", round(float(_np.corrcoef(d3, wb)[0, 1]), 3),
+          " corr(done-plan, units) =", round(float(_np.corrcoef(d3, wu)[0, 1]), 3))
+    slow = _np.argsort(-d3)[:5]
+    print("slowest warps (cta, warp, us after plan, bytes, units):",
+          [(int(i // nw), int(i % nw), round(float(d3[i]), 1), int(wb[i]), int(wu[i])) for i in slow])
+    a[:, 0] = a[:, 1] - 5000
+elif os.environ.get("B64_TRACE_FM"):
     fm = a[:, 0] >> 32
     tm = a[:, 0] & 0xFFFFFFFF
     print("first_msg mismatches:", int((fm != tm).sum()))
