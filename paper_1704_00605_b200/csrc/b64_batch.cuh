@@ -339,14 +339,28 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const int64_t i_lo = blockIdx.x * chunk < k ? blockIdx.x * chunk : k;
   const int64_t i_hi = i_lo + chunk < k ? i_lo + chunk : k;
   int64_t tot_o = 0, tot_u = 0;
+  // a CTA's messages usually fit one round: keep that round's values in
+  // registers so pass 2 needs no reloads (in_off, pad characters) and no scan
+  const bool one_round = i_hi - i_lo <= kBThreads;
+  int64_t c_a = 0, c_b = 0, c_o = 0, c_u = 0, c_po = 0, c_pu = 0;
   for (int64_t r0 = i_lo; r0 < i_hi; r0 += kBThreads) {
     const int64_t i = r0 + tid;
-    int64_t o = 0, u = 0;
-    if (i < i_hi) msg_sizes<DECODE>(in, in_off[i], in_off[i + 1], o, u, flags);
+    int64_t o = 0, u = 0, a = 0, b = 0;
+    if (i < i_hi) {
+      a = in_off[i];
+      b = in_off[i + 1];
+      msg_sizes<DECODE>(in, a, b, o, u, flags);
+    }
     int64_t po, pu, to, tu;
     block_exclusive_scan2(o, u, po, pu, to, tu, sh);
     tot_o += to;
     tot_u += tu;
+    c_a = a;
+    c_b = b;
+    c_o = o;
+    c_u = u;
+    c_po = po;
+    c_pu = pu;
   }
   if (tid == 0) {
     blk[2 * blockIdx.x] = tot_o;
@@ -374,14 +388,17 @@ __global__ void __launch_bounds__(kBThreads, 1)
   }
   for (int64_t r0 = i_lo; r0 < i_hi; r0 += kBThreads) {
     const int64_t i = r0 + tid;
-    int64_t o = 0, u = 0, a = 0, b = 0;
-    if (i < i_hi) {
-      a = in_off[i];
-      b = in_off[i + 1];
-      msg_sizes<DECODE>(in, a, b, o, u, flags);
+    int64_t o = c_o, u = c_u, a = c_a, b = c_b;
+    int64_t po = c_po, pu = c_pu, to = tot_o, tu = tot_u;
+    if (!one_round) {
+      o = u = a = b = 0;
+      if (i < i_hi) {
+        a = in_off[i];
+        b = in_off[i + 1];
+        msg_sizes<DECODE>(in, a, b, o, u, flags);
+      }
+      block_exclusive_scan2(o, u, po, pu, to, tu, sh);
     }
-    int64_t po, pu, to, tu;
-    block_exclusive_scan2(o, u, po, pu, to, tu, sh);
     if (i < i_hi) {
       out_off[i] = bo + po;
       unit_off[i] = bu + pu;
