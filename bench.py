@@ -489,14 +489,32 @@ def run_small_configs(args):
         dec_ms = timed(dec, "decode")
         if os.environ.get("B64_BENCH_NOCHECK") != "1":
             assert int(y_st.abs().sum().item()) == 0 and torch.equal(y[:tot], raw)
-        ms = enc_ms + dec_ms
+        # one step = batched encode then batched decode, replayed as one CUDA graph
+        gs = torch.cuda.Stream()
+        with torch.cuda.stream(gs):
+            b64.b64_encode_batch(raw, doff, out=out, out_off=out_off, ws=wse, stream=gs)
+            b64.b64_decode_batch(out, out_off, out=y, out_off=y_off, out_len=y_len, err_pos=y_err,
+                                 status=y_st, ws=wsd, total_in=mt, stream=gs)
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            b64.b64_encode_batch(raw, doff, out=out, out_off=out_off, ws=wse, stream=gs)
+            b64.b64_decode_batch(out, out_off, out=y, out_off=y_off, out_len=y_len, err_pos=y_err,
+                                 status=y_st, ws=wsd, total_in=mt, stream=gs)
+        y.zero_()
+        graph_ms = timed(graph.replay, "graph_replay")
+        if os.environ.get("B64_BENCH_NOCHECK") != "1":
+            assert int(y_st.abs().sum().item()) == 0 and torch.equal(y[:tot], raw)
+        ms = graph_ms
         value = (tot + mt) / (ms / 1e3) / 1e9
         algo = {"encode": tot + mt + 16 * (k + 1), "decode": mt + tot + 16 * (k + 1) + 20 * k}
-        detail = {"encode_ms": enc_ms, "decode_ms": dec_ms, "messages": k, "raw_bytes": tot, "text_bytes": mt,
+        detail = {"encode_ms": enc_ms, "decode_ms": dec_ms, "graph_replay_ms": graph_ms, "messages": k,
+                  "raw_bytes": tot, "text_bytes": mt,
                   "encode_GBps_input": tot / (enc_ms / 1e3) / 1e9, "decode_GBps_input": mt / (dec_ms / 1e3) / 1e9}
         dom, dom_ms = ("encode", enc_ms) if enc_ms >= dec_ms else ("decode", dec_ms)
-        desc = "C2: 10,000 messages, log-uniform 100 B - 64 KiB (seed 1): batched encode + batched decode (incl. planner)"
-        launches = 4
+        desc = ("C2: 10,000 messages, log-uniform 100 B - 64 KiB (seed 1): batched encode + batched decode "
+                "(incl. planner); step = one CUDA-graph replay of the two calls")
+        launches = 2
     elif wl == "despace":
         # f3: 1 GiB of MIME-style text (76-char lines + CRLF, 2.6 % whitespace),
         # built on the device from C3-seeded bytes with our encoder + a view.
