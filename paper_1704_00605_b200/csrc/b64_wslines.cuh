@@ -26,7 +26,8 @@
 
 namespace b64 {
 
-constexpr int kWlThreads = 512;
+constexpr int kWlWarps = 16;                       // compute warps
+constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #ifndef B64_WL_TILE
 #define B64_WL_TILE 28672
 #endif
@@ -36,7 +37,10 @@ constexpr int kWlThreads = 512;
 constexpr int kWlTile = B64_WL_TILE;    // max input bytes per tile (whole lines)
 constexpr int kWlStages = B64_WL_STAGES;
 constexpr int kWlMaxLine = 4092;      // longest line the fast path takes
-constexpr int kWlOut = kWlTile / 4 * 3 + 64;
+// per-warp output slice: a warp owns a contiguous range of <= ceil(quads/16)
+// quads of a tile, rounded up to whole 32-quad rows
+constexpr int kWlWarpQuads = ((kWlTile / 4 + kWlWarps - 1) / kWlWarps + 31) / 32 * 32;
+constexpr int kWlSlice = 3 * kWlWarpQuads + 48;
 
 // Per-call state in the caller's workspace (zeroed by a 16-byte memset
 // before the launch).
@@ -49,8 +53,9 @@ struct WlState {
 
 struct alignas(128) WlSmem {
   uint8_t in[kWlStages][kWlTile + 64];
-  alignas(16) uint8_t out[2][kWlOut];
+  alignas(16) uint8_t out[kWlWarps][kWlSlice];
   uint64_t full[kWlStages];
+  uint64_t empty[kWlStages];
   int64_t geo[4];   // Mc (kept chars), nlines, ok
   int32_t Le[2];    // L, e
   int32_t flag;
@@ -64,7 +69,10 @@ __global__ void __launch_bounds__(kWlThreads, 2)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < 256) g_dec_tab[tid] = kInvalid;
   if (tid == 0) {
-    for (int s = 0; s < kWlStages; ++s) ptx::mbar_init(&S.full[s], 1);
+    for (int s = 0; s < kWlStages; ++s) {
+      ptx::mbar_init(&S.full[s], 1);
+      ptx::mbar_init(&S.empty[s], kWlWarps);
+    }
     ptx::fence_mbar_init();
     S.flag = 0;
   }
@@ -125,121 +133,146 @@ __global__ void __launch_bounds__(kWlThreads, 2)
     const int64_t Q = Mc / 4;                             // complete quads
     const bool pads_ok = (Mc & 3) == 0;
     const uint32_t inv = G > 1 ? static_cast<uint32_t>(((1ull << 32) + G - 1) / G) : 0u;
-    const uint64_t pol = ptx::policy_evict_first();
-    auto load = [&](int64_t t, int s) {
-      const int64_t src = t * Lt * static_cast<int64_t>(Sl);
-      const int64_t len = M - src < static_cast<int64_t>(Lt) * Sl ? M - src : static_cast<int64_t>(Lt) * Sl;
-      const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src);
-      const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
-      const uintptr_t g1 = (g + static_cast<uintptr_t>(len) + 15) & ~static_cast<uintptr_t>(15);
-      ptx::mbar_arrive_expect_tx(&S.full[s], static_cast<uint32_t>(g1 - g0));
-      ptx::bulk_g2s(S.in[s], reinterpret_cast<const void *>(g0), static_cast<uint32_t>(g1 - g0),
-                    &S.full[s], pol);
+    auto line_of = [&](int q) -> int {
+      return G == 1 ? q : static_cast<int>(__umulhi(static_cast<uint32_t>(q), inv));
     };
-    const int64_t t0 = blockIdx.x;
-    if (tid == 0)
-      for (int k = 0; k < kWlStages - 1 && t0 + static_cast<int64_t>(k) * gridDim.x < ntiles; ++k)
-        load(t0 + static_cast<int64_t>(k) * gridDim.x, k);
-    const uint32_t eolw = e == 2 ? 0x0A0Du : 0x0Au, eolm = e == 2 ? 0xFFFFu : 0xFFu;
-    // thread-invariant walk of an interior tile: quad tid + 512 k
-    const int line_t = tid / G, col_t = tid % G;
-    const int p_t = line_t * Sl + 4 * col_t;
-    const int dc = kWlThreads % G;
-    const int pstep = (kWlThreads / G) * Sl + 4 * dc;
-    int it = 0;
-    for (int64_t t = t0; t < ntiles; t += gridDim.x, ++it) {
-      const int s = it % kWlStages, so = it & 1;
-      if (tid == 0 && t + (kWlStages - 1) * static_cast<int64_t>(gridDim.x) < ntiles)
-        load(t + (kWlStages - 1) * static_cast<int64_t>(gridDim.x), (it + kWlStages - 1) % kWlStages);
-      const int64_t src = t * Lt * static_cast<int64_t>(Sl);
-      const int64_t q0 = t * Lt * static_cast<int64_t>(G);     // first quad of the tile
-      const int64_t line0 = t * Lt;
-      const int64_t q1 = q0 + static_cast<int64_t>(Lt) * G < Q ? q0 + static_cast<int64_t>(Lt) * G : Q;
-      const int nq = static_cast<int>(q1 - q0);
-      const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src)) & 15);
-      uint8_t *gdst = out + 3 * q0;
-      const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
-      uint8_t *ob = S.out[so] + omis;
-      const uint32_t *win = reinterpret_cast<const uint32_t *>(S.in[s]);
-      ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kWlStages) & 1));
-      if (viol) continue;  // drain the loads in flight, skip the work
-      uint32_t bad = 0;
-      if (q1 < Q && (line0 + Lt) * static_cast<int64_t>(Sl) <= M && Q - q1 >= 1) {
-        // Interior tile: Lt whole lines, each followed by its EOL, no final
-        // quad.  The tile starts on a line boundary and the stride is 512
-        // quads, so each thread's (column, offset) walk is tile-invariant
-        // up to the window misalignment: one increment per quad.
-        // the EOL of every line of the tile: one check per line, off the quad loop
-        for (int ln = tid; ln < Lt; ln += kWlThreads) {
-          const int b = imis + ln * Sl + L;
-          const uint32_t x = __funnelshift_r(win[b >> 2], win[(b >> 2) + 1], 8 * (b & 3));
-          if ((x & eolm) != eolw) bad |= 0x80u;
+    if (warp == kWlWarps) {
+      // ---- producer: lane 0 streams whole-line tiles into the ring
+      if (lane == 0) {
+        const uint64_t pol = ptx::policy_evict_first();
+        int k = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+          const int s = k % kWlStages;
+          if (k >= kWlStages) ptx::mbar_wait(&S.empty[s], static_cast<uint32_t>((k / kWlStages - 1) & 1));
+          const int64_t src = t * Lt * static_cast<int64_t>(Sl);
+          const int64_t tl = static_cast<int64_t>(Lt) * Sl;
+          const int64_t len = M - src < tl ? M - src : tl;
+          const uintptr_t g = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src);
+          const uintptr_t g0 = g & ~static_cast<uintptr_t>(15);
+          const uintptr_t g1 = (g + static_cast<uintptr_t>(len) + 15) & ~static_cast<uintptr_t>(15);
+          ptx::mbar_arrive_expect_tx(&S.full[s], static_cast<uint32_t>(g1 - g0));
+          ptx::bulk_g2s(S.in[s], reinterpret_cast<const void *>(g0), static_cast<uint32_t>(g1 - g0),
+                        &S.full[s], pol);
         }
-        int a = imis + p_t, col = col_t, o = 3 * tid;
-        for (int ql = tid; ql < nq; ql += kWlThreads) {
-          const uint32_t w = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
-          const uint32_t v0 = lds_u8((w & 0xFFu) | tb);
-          const uint32_t v1 = lds_u8(__byte_perm(w, tb, 0x7651));
-          const uint32_t v2 = lds_u8(__byte_perm(w, tb, 0x7652));
-          const uint32_t v3 = lds_u8(__byte_perm(w, tb, 0x7653));
-          bad |= v0 | v1 | v2 | v3;
-          const uint32_t V = ((v0 * 64u + v1) * 64u + v2) * 64u + v3;
-          uint8_t *p = ob + o;
-          p[0] = static_cast<uint8_t>(V >> 16);
-          p[1] = static_cast<uint8_t>(V >> 8);
-          p[2] = static_cast<uint8_t>(V);
-          a += pstep;
-          o += 3 * kWlThreads;
-          col += dc;
-          if (col >= G) {
-            col -= G;
-            a += e;
-          }
-        }
-      } else {  // first / last tiles: generic walk, final quad, partial last line
-        for (int ql = tid; ql < nq; ql += kWlThreads) {
-          const uint32_t line =
-              G == 1 ? static_cast<uint32_t>(ql) : __umulhi(static_cast<uint32_t>(ql), inv);
-          const int col = ql - static_cast<int>(line) * G;
-          const int a = imis + static_cast<int>(line) * Sl + 4 * col;
-          const uint32_t w = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
-          uint32_t v0 = lds_u8((w & 0xFFu) | tb);
-          uint32_t v1 = lds_u8(__byte_perm(w, tb, 0x7651));
-          uint32_t v2 = lds_u8(__byte_perm(w, tb, 0x7652));
-          uint32_t v3 = lds_u8(__byte_perm(w, tb, 0x7653));
-          if (pads_ok && q0 + ql == Q - 1) {  // the final quad: '=' at the last two positions (R-pad)
-            const uint32_t c2 = (w >> 16) & 0xFFu, c3 = w >> 24;
-            if (c3 == '=') {
-              v3 = 0;
-              if (c2 == '=') v2 = 0;
+      }
+    } else {
+      // ---- compute warps: each owns a contiguous range of the tile's quads
+      // and writes its bytes itself (no CTA-wide barrier per tile)
+      const uint32_t eolw = e == 2 ? 0x0A0Du : 0x0Au, eolm = e == 2 ? 0xFFFFu : 0xFFu;
+      const int dl32 = 32 / G, dc32 = 32 % G;
+      const int pstep = dl32 * Sl + 4 * dc32;
+      uint8_t *slice = S.out[warp];
+      int k = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int s = k % kWlStages;
+        ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((k / kWlStages) & 1));
+        int stop = 0;
+        if (lane == 0) stop = S.flag | *reinterpret_cast<volatile int32_t *>(&st->viol);
+        stop = __shfl_sync(0xffffffffu, stop, 0);
+        if (!stop) {
+          const int64_t src = t * Lt * static_cast<int64_t>(Sl);
+          const int64_t q0 = t * Lt * static_cast<int64_t>(G);   // first quad of the tile
+          const int64_t line0 = t * Lt;
+          const int64_t q1 = q0 + static_cast<int64_t>(Lt) * G < Q ? q0 + static_cast<int64_t>(Lt) * G : Q;
+          const int nq = static_cast<int>(q1 - q0);
+          int per = (nq + kWlWarps - 1) / kWlWarps;
+          per = (per + 31) & ~31;
+          const int qa = warp * per < nq ? warp * per : nq;
+          const int qb = qa + per < nq ? qa + per : nq;
+          const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src)) & 15);
+          const uint32_t *win = reinterpret_cast<const uint32_t *>(S.in[s]);
+          uint8_t *gdst = out + 3 * (q0 + qa);
+          const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
+          uint8_t *ob = slice + omis - 3 * qa;  // quad q -> ob + 3q
+          uint32_t bad = 0;
+          const bool interior = q1 < Q && (line0 + Lt) * static_cast<int64_t>(Sl) <= M;
+          if (interior && qa < qb) {
+            // all lines full with an EOL, no final quad: incremental walk
+            int q = qa + lane;
+            int ln = line_of(q), col = q - ln * G;
+            int a = imis + ln * Sl + 4 * col;
+            for (; q < qb; q += 32) {
+              const uint32_t w = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+              const uint32_t v0 = lds_u8((w & 0xFFu) | tb);
+              const uint32_t v1 = lds_u8(__byte_perm(w, tb, 0x7651));
+              const uint32_t v2 = lds_u8(__byte_perm(w, tb, 0x7652));
+              const uint32_t v3 = lds_u8(__byte_perm(w, tb, 0x7653));
+              bad |= v0 | v1 | v2 | v3;
+              const uint32_t V = ((v0 * 64u + v1) * 64u + v2) * 64u + v3;
+              uint8_t *p = ob + 3 * q;
+              p[0] = static_cast<uint8_t>(V >> 16);
+              p[1] = static_cast<uint8_t>(V >> 8);
+              p[2] = static_cast<uint8_t>(V);
+              a += pstep;
+              col += dc32;
+              if (col >= G) {
+                col -= G;
+                a += e;
+              }
+            }
+          } else {
+            for (int q = qa + lane; q < qb; q += 32) {
+              const int ln = line_of(q);
+              const int col = q - ln * G;
+              const int a = imis + ln * Sl + 4 * col;
+              const uint32_t w = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+              uint32_t v0 = lds_u8((w & 0xFFu) | tb);
+              uint32_t v1 = lds_u8(__byte_perm(w, tb, 0x7651));
+              uint32_t v2 = lds_u8(__byte_perm(w, tb, 0x7652));
+              uint32_t v3 = lds_u8(__byte_perm(w, tb, 0x7653));
+              if (pads_ok && q0 + q == Q - 1) {  // the final quad: '=' at the last two positions (R-pad)
+                const uint32_t c2 = (w >> 16) & 0xFFu, c3 = w >> 24;
+                if (c3 == '=') {
+                  v3 = 0;
+                  if (c2 == '=') v2 = 0;
+                }
+              }
+              bad |= v0 | v1 | v2 | v3;
+              const uint32_t V = ((v0 * 64u + v1) * 64u + v2) * 64u + v3;
+              uint8_t *p = ob + 3 * q;
+              p[0] = static_cast<uint8_t>(V >> 16);
+              p[1] = static_cast<uint8_t>(V >> 8);
+              p[2] = static_cast<uint8_t>(V);
             }
           }
-          bad |= v0 | v1 | v2 | v3;
-          const uint32_t V = ((v0 * 64u + v1) * 64u + v2) * 64u + v3;
-          uint8_t *p = ob + 3 * ql;
-          p[0] = static_cast<uint8_t>(V >> 16);
-          p[1] = static_cast<uint8_t>(V >> 8);
-          p[2] = static_cast<uint8_t>(V);
-          // end of a line with an EOL after it: verify the EOL bytes
-          if (col == G - 1 && (line0 + static_cast<int64_t>(line) + 1) * Sl <= M) {
-            const int b = a + 4;
+          // EOL of every line whose last quad this warp owns (and that has one)
+          for (int ln = qa / G + lane; ln < qb / G; ln += 32) {
+            if ((line0 + ln + 1) * Sl > M) break;
+            const int b = imis + ln * Sl + L;
             const uint32_t x = __funnelshift_r(win[b >> 2], win[(b >> 2) + 1], 8 * (b & 3));
             if ((x & eolm) != eolw) bad |= 0x80u;
           }
+          if (__any_sync(0xffffffffu, bad & 0x80u)) {
+            if (lane == 0) {
+              S.flag = 1;
+              atomicExch(&st->viol, 1);
+            }
+          } else if (qa < qb) {
+            // this warp's bytes: congruent staging -> 16-byte stores + byte edges
+            __syncwarp();
+            const int n = 3 * (qb - qa);
+            const uint8_t *src8 = slice + omis;
+            const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
+            const uintptr_t ga = (g + 15) & ~static_cast<uintptr_t>(15);
+            const uintptr_t gb = (g + static_cast<uintptr_t>(n)) & ~static_cast<uintptr_t>(15);
+            if (gb > ga) {
+              const int head = static_cast<int>(ga - g), ng = static_cast<int>((gb - ga) >> 4);
+              for (int i = lane; i < ng; i += 32)
+                *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(ga) + 16 * i) =
+                    ptx::lds128(src8 + head + 16 * i);
+              const int tail0 = static_cast<int>(gb - g);
+              if (lane < head) gdst[lane] = src8[lane];
+              if (lane >= 16 && lane - 16 < n - tail0) gdst[tail0 + lane - 16] = src8[tail0 + lane - 16];
+            } else {
+              for (int i = lane; i < n; i += 32) gdst[i] = src8[i];
+            }
+          }
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&S.empty[s]);
       }
-      if (bad & 0x80u) S.flag = 1;  // benign race: any writer sets it
-      if (tid == 0 && *reinterpret_cast<volatile int32_t *>(&st->viol)) S.flag = 1;
-      ptx::fence_proxy_async_smem();
-      __syncthreads();
-      if (S.flag) {  // give up (every later tile of this CTA is only drained)
-        viol = true;
-        if (tid == 0) atomicExch(&st->viol, 1);
-        continue;
-      }
-      // (the pad bytes of the final quad are copied too: beyond out_len, within capacity)
-      cta_copy_out_congruent(gdst, ob, 3 * nq);
     }
+    viol = S.flag != 0;
   }
   // ---- last CTA out: the verdict and, on success, the result record
   __syncthreads();
