@@ -37,6 +37,9 @@ namespace b64 {
 #ifndef B64_SKELETON  // measurement only: move the bytes, skip the transform
 #define B64_SKELETON 0
 #endif
+#ifndef B64_DEC_STG32  // measurement only: decode DIRECT tiles store from registers
+#define B64_DEC_STG32 0
+#endif
 #ifndef B64_STORE_EVICT_FIRST
 #define B64_STORE_EVICT_FIRST 0
 #endif
@@ -374,6 +377,15 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
     o[0] = __byte_perm(V[0], V[1], 0x6012);
     o[1] = __byte_perm(V[1], V[2], 0x5601);
     o[2] = __byte_perm(V[2], V[3], 0x4560);
+#if B64_DEC_STG32
+    if constexpr (DIRECT) {  // measurement variant: three 4-byte stores straight from registers
+      uint32_t *g = reinterpret_cast<uint32_t *>(gdst + bo);
+      g[0] = o[0];
+      g[1] = o[1];
+      g[2] = o[2];
+      continue;
+    }
+#endif
     store_words<(OA >= 4 ? 4 : 1), 3>(sout + bo, o, active, lane);
     if constexpr (DIRECT) {
       __syncwarp();

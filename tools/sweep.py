@@ -59,6 +59,7 @@ VARIANTS = {
     "b_p2_w32_skel": {"B64_BATCH_PASSES": 2, "B64_BATCH_WARPS": 32, "B64_SKELETON": 1},
     "b_w20": {"B64_BATCH_WARPS": 20},
     "b_trace": {"B64_BATCH_TRACE": 1},
+    "dec_stg32": {"B64_DEC_STG32": 1},
     "b_p6_s3": {"B64_BATCH_PASSES": 6, "B64_BATCH_SLOTS": 3},
     "b_p8_s3": {"B64_BATCH_PASSES": 8, "B64_BATCH_SLOTS": 3},
     "b_p4_s3": {"B64_BATCH_SLOTS": 3},
