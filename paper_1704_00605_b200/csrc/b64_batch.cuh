@@ -312,7 +312,6 @@ __global__ void __launch_bounds__(kBThreads, 1)
                  int32_t *__restrict__ status, int32_t *__restrict__ first_msg, int flags) {
   using Ring = typename std::conditional<DECODE, DecRing, EncRing>::type;
   constexpr int UIN = DECODE ? DU::kIn : EU::kIn;
-  constexpr int UOUT = DECODE ? DU::kOut : EU::kOut;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ int64_t sh[66];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
