@@ -464,6 +464,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #endif
   wc = wi;
 
+#if B64_BATCH_PREFETCH
+  const uintptr_t in_end = reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(in_off[k]);
+#endif
   auto issue = [&](int64_t u) {
     const UnitDesc d = wi.seek(u, k, in_off, out_off, unit_off, lane);
     if (lane == 0) {
@@ -474,6 +477,12 @@ __global__ void __launch_bounds__(kBThreads, 1)
           (static_cast<uint32_t>(g & 15) + static_cast<uint32_t>(d.len) + 15u) & ~15u;
       mbar_arrive_expect_tx(&R.full[s], bytes);
       bulk_g2s(R.in[s], reinterpret_cast<const void *>(g0), bytes, &R.full[s], pol);
+#if B64_BATCH_PREFETCH
+      // units are contiguous in the input: warm L2 with the bytes this warp
+      // reads B64_BATCH_PREFETCH units further on (beyond the smem ring)
+      const uintptr_t pf = g0 + static_cast<uintptr_t>(B64_BATCH_PREFETCH) * UIN;
+      if (pf + UIN <= in_end) bulk_prefetch_l2(reinterpret_cast<const void *>(pf), UIN);
+#endif
     }
   };
 

@@ -28,6 +28,9 @@ namespace b64 {
 #ifndef B64_BATCH_SLOTS   // per-warp input ring depth (batched)
 #define B64_BATCH_SLOTS 4
 #endif
+#ifndef B64_BATCH_PREFETCH  // batched: L2 prefetch distance in units (0 = off)
+#define B64_BATCH_PREFETCH 0
+#endif
 #ifndef B64_BATCH_WARPS   // warps per CTA (batched)
 #define B64_BATCH_WARPS 16
 #endif

@@ -60,6 +60,9 @@ VARIANTS = {
     "b_w20": {"B64_BATCH_WARPS": 20},
     "b_trace": {"B64_BATCH_TRACE": 1},
     "dec_stg32": {"B64_DEC_STG32": 1},
+    "b_pf4": {"B64_BATCH_PREFETCH": 4},
+    "b_pf8": {"B64_BATCH_PREFETCH": 8},
+    "b_pf12": {"B64_BATCH_PREFETCH": 12},
     "b_p6_s3": {"B64_BATCH_PASSES": 6, "B64_BATCH_SLOTS": 3},
     "b_p8_s3": {"B64_BATCH_PASSES": 8, "B64_BATCH_SLOTS": 3},
     "b_p4_s3": {"B64_BATCH_SLOTS": 3},
