@@ -45,6 +45,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, uint32
       : "memory");
 }
 
+// Producer-side wait with a sleep back-off: test_wait, then __nanosleep
+// between polls, so an idle producer warp does not take issue slots from
+// the compute warps of its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(ns);
+  }
+}
+
 // Consumer-side wait: plain try_wait loop (no suspend hint), the data
 // normally lands within a few hundred cycles of being needed.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {

@@ -31,6 +31,9 @@ constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #ifndef B64_WL_TILE
 #define B64_WL_TILE 28672
 #endif
+#ifndef B64_WL_SLEEP  // producer back-off between empty-slot polls (ns); 0 = try_wait loop
+#define B64_WL_SLEEP 0
+#endif
 #ifndef B64_WL_STAGES
 #define B64_WL_STAGES 2
 #endif
@@ -143,7 +146,12 @@ __global__ void __launch_bounds__(kWlThreads, 2)
         int k = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
           const int s = k % kWlStages;
-          if (k >= kWlStages) ptx::mbar_wait(&S.empty[s], static_cast<uint32_t>((k / kWlStages - 1) & 1));
+          if (k >= kWlStages) {
+            if (B64_WL_SLEEP > 0)
+              ptx::mbar_wait_sleep(&S.empty[s], static_cast<uint32_t>((k / kWlStages - 1) & 1), B64_WL_SLEEP);
+            else
+              ptx::mbar_wait(&S.empty[s], static_cast<uint32_t>((k / kWlStages - 1) & 1));
+          }
           const int64_t src = t * Lt * static_cast<int64_t>(Sl);
           const int64_t tl = static_cast<int64_t>(Lt) * Sl;
           const int64_t len = M - src < tl ? M - src : tl;
@@ -191,6 +199,7 @@ __global__ void __launch_bounds__(kWlThreads, 2)
             int q = qa + lane;
             int ln = line_of(q), col = q - ln * G;
             int a = imis + ln * Sl + 4 * col;
+            uint8_t *po = ob + 3 * q;
             for (; q < qb; q += 32) {
               const uint32_t w = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
               const uint32_t v0 = lds_u8((w & 0xFFu) | tb);
@@ -199,10 +208,10 @@ __global__ void __launch_bounds__(kWlThreads, 2)
               const uint32_t v3 = lds_u8(__byte_perm(w, tb, 0x7653));
               bad |= v0 | v1 | v2 | v3;
               const uint32_t V = ((v0 * 64u + v1) * 64u + v2) * 64u + v3;
-              uint8_t *p = ob + 3 * q;
-              p[0] = static_cast<uint8_t>(V >> 16);
-              p[1] = static_cast<uint8_t>(V >> 8);
-              p[2] = static_cast<uint8_t>(V);
+              po[0] = static_cast<uint8_t>(V >> 16);
+              po[1] = static_cast<uint8_t>(V >> 8);
+              po[2] = static_cast<uint8_t>(V);
+              po += 96;
               a += pstep;
               col += dc32;
               if (col >= G) {

@@ -61,6 +61,10 @@ VARIANTS = {
     "b_trace": {"B64_BATCH_TRACE": 1},
     "dec_stg32": {"B64_DEC_STG32": 1},
     "b_pf4": {"B64_BATCH_PREFETCH": 4},
+    "wl_sleep0": {"B64_WL_SLEEP": 0},
+    "wl_sleep64": {"B64_WL_SLEEP": 64},
+    "wl_sleep256": {"B64_WL_SLEEP": 256},
+    "wl_s3_24k": {"B64_WL_SLEEP": 0, "B64_WL_TILE": 24576, "B64_WL_STAGES": 3},
     "b_pf8": {"B64_BATCH_PREFETCH": 8},
     "b_pf12": {"B64_BATCH_PREFETCH": 12},
     "b_p6_s3": {"B64_BATCH_PASSES": 6, "B64_BATCH_SLOTS": 3},
