@@ -40,6 +40,9 @@ namespace b64 {
 #ifndef B64_SKELETON  // measurement only: move the bytes, skip the transform
 #define B64_SKELETON 0
 #endif
+#ifndef B64_ENC_ARITH  // measurement only: Table I mapping by SWAR arithmetic instead of the table
+#define B64_ENC_ARITH 0
+#endif
 #ifndef B64_DEC_STG32  // measurement only: decode DIRECT tiles store from registers
 #define B64_DEC_STG32 0
 #endif
@@ -206,6 +209,27 @@ __device__ __forceinline__ void st_global_v4(uint8_t *p, const uint4 &v) {
 // OR-ed into the table base (SHF + LOP3, or one LOP3 / LEA.HI).
 template <bool TOPZERO>
 __device__ __forceinline__ uint32_t enc_group(uint32_t x, uint32_t tb) {
+#if B64_ENC_ARITH
+  // Table I (with the f1 alphabet's 62 / 63) as per-byte SWAR arithmetic on
+  // the four packed fields v (< 64): v + 65, + 6 from 26, - 75 from 52,
+  // - d62 at 62, + d63 at 63 (the paper's range-offset mapping); each
+  // partial sum stays in 0..255 per byte, so no carry or borrow crosses
+  // bytes.  d62 / d63 come from the launch's table entries 62 / 63.
+  const uint32_t v = ((x >> 18) & 0x3Fu) | ((x >> 4) & 0x3F00u) | ((x << 10) & 0x3F0000u) |
+                     ((x << 24) & 0x3F000000u);
+  const uint32_t c62 = lds_u8(tb | 62u), c63 = lds_u8(tb | 63u);
+  const uint32_t d62 = 58u - c62, d63 = c63 - 59u + d62;
+  uint32_t r = v + 0x41414141u;
+  const uint32_t g26 = ((v + 0x66666666u) >> 7) & 0x01010101u;
+  const uint32_t g52 = ((v + 0x4C4C4C4Cu) >> 7) & 0x01010101u;
+  const uint32_t g62 = ((v + 0x42424242u) >> 7) & 0x01010101u;
+  const uint32_t g63 = (r >> 7) & 0x01010101u;
+  r += g26 * 6u;
+  r -= g52 * 75u;
+  r -= g62 * d62;
+  r += g63 * d63;
+  return r;
+#endif
   const uint32_t a0 = TOPZERO ? ((x >> 18) | tb) : (((x >> 18) & 63u) | tb);
   const uint32_t a1 = ((x >> 12) & 63u) | tb;
   const uint32_t a2 = ((x >> 6) & 63u) | tb;
