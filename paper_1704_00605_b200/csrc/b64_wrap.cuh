@@ -28,6 +28,9 @@ constexpr int kWrThreads = 512;
 #ifndef B64_WR_OUT
 #define B64_WR_OUT 28672
 #endif
+#ifndef B64_WR_BATCH  // fast path: groups per thread whose loads are issued together (0 = off)
+#define B64_WR_BATCH 2
+#endif
 #ifndef B64_WR_STAGES
 #define B64_WR_STAGES 2
 #endif
@@ -150,8 +153,40 @@ __global__ void __launch_bounds__(kWrThreads, 2)
       const uint32_t *wp = win + (a_t >> 2);
       uint8_t *p = ob + p_t;
       int col = col_t;
+      int g = tid;
+#if B64_WR_BATCH
+      // B64_WR_BATCH groups per step: every input / table load of the batch
+      // is issued before its first store (the compiler does not move shared
+      // loads above shared stores of the previous group on its own).
+      constexpr int NB = B64_WR_BATCH;
+      for (; g + (NB - 1) * kWrThreads < ngrp; g += NB * kWrThreads) {
+        uint8_t *pb[NB];
+        bool lb[NB];
+        uint32_t x[NB], c[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          x[j] = __funnelshift_r(wp[0], wp[1], sh_t);
+          pb[j] = p;
+          lb[j] = col == W.G - 1;
+          wp += 3 * kWrThreads / 4;
+          p += pstep;
+          col += dc;
+          if (col >= W.G) {
+            col -= W.G;
+            p += E;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NB; ++j) c[j] = enc_group<true>(__byte_perm(x[j], 0u, 0x4012), tb);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          store4<U16>(pb[j], c[j]);
+          if (lb[j]) store_eol<U16, E>(pb[j] + 4);
+        }
+      }
+#endif
 #pragma unroll 4
-      for (int g = tid; g < ngrp; g += kWrThreads) {
+      for (; g < ngrp; g += kWrThreads) {
         const uint32_t x = __funnelshift_r(wp[0], wp[1], sh_t);
         const uint32_t c = enc_group<true>(__byte_perm(x, 0u, 0x4012), tb);
         store4<U16>(p, c);

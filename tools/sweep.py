@@ -47,6 +47,10 @@ VARIANTS = {
     "skel_w16_c1_in3": {"B64_SKELETON": 1, "B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1, "B64_STAGES_IN": 3},
     # batched (C2) variants
     "b_plan_only": {"B64_BATCH_PLAN_ONLY": 1},
+    "wr_b0": {"B64_WR_BATCH": 0},
+    "wr_b4": {"B64_WR_BATCH": 4},
+    "wr_b2": {"B64_WR_BATCH": 2},
+    "wr_b8": {"B64_WR_BATCH": 8},
     "enc_arith": {"B64_ENC_ARITH": 1},
     "b_p2": {"B64_BATCH_PASSES": 2},
     "b_p8": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8},
