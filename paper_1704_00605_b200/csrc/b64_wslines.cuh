@@ -34,6 +34,9 @@ constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #ifndef B64_WL_SLEEP  // producer back-off between empty-slot polls (ns); 0 = try_wait loop
 #define B64_WL_SLEEP 0
 #endif
+#ifndef B64_WL_BATCH  // interior loop: quads per thread whose loads are issued together (0 = off)
+#define B64_WL_BATCH 6
+#endif
 #ifndef B64_WL_STAGES
 #define B64_WL_STAGES 2
 #endif
@@ -200,6 +203,43 @@ __global__ void __launch_bounds__(kWlThreads, 2)
             int ln = line_of(q), col = q - ln * G;
             int a = imis + ln * Sl + 4 * col;
             uint8_t *po = ob + 3 * q;
+#if B64_WL_BATCH
+            // B64_WL_BATCH quads per step, loads ahead of stores (as in the
+            // wrapped encoder)
+            constexpr int NB = B64_WL_BATCH;
+            for (; q + 32 * (NB - 1) < qb; q += 32 * NB) {
+              uint32_t wv[NB];
+              uint8_t *pp[NB];
+#pragma unroll
+              for (int j = 0; j < NB; ++j) {
+                wv[j] = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+                pp[j] = po;
+                po += 96;
+                a += pstep;
+                col += dc32;
+                if (col >= G) {
+                  col -= G;
+                  a += e;
+                }
+              }
+              uint32_t vv[NB][4];
+#pragma unroll
+              for (int j = 0; j < NB; ++j) {
+                vv[j][0] = lds_u8((wv[j] & 0xFFu) | tb);
+                vv[j][1] = lds_u8(__byte_perm(wv[j], tb, 0x7651));
+                vv[j][2] = lds_u8(__byte_perm(wv[j], tb, 0x7652));
+                vv[j][3] = lds_u8(__byte_perm(wv[j], tb, 0x7653));
+              }
+#pragma unroll
+              for (int j = 0; j < NB; ++j) {
+                bad |= vv[j][0] | vv[j][1] | vv[j][2] | vv[j][3];
+                const uint32_t V = ((vv[j][0] * 64u + vv[j][1]) * 64u + vv[j][2]) * 64u + vv[j][3];
+                pp[j][0] = static_cast<uint8_t>(V >> 16);
+                pp[j][1] = static_cast<uint8_t>(V >> 8);
+                pp[j][2] = static_cast<uint8_t>(V);
+              }
+            }
+#endif
             for (; q < qb; q += 32) {
               const uint32_t w = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
               const uint32_t v0 = lds_u8((w & 0xFFu) | tb);

@@ -48,6 +48,12 @@ VARIANTS = {
     # batched (C2) variants
     "b_plan_only": {"B64_BATCH_PLAN_ONLY": 1},
     "wr_b0": {"B64_WR_BATCH": 0},
+    "wl_b0": {"B64_WL_BATCH": 0},
+    "wl_b4": {"B64_WL_BATCH": 4},
+    "wl_b8": {"B64_WL_BATCH": 8},
+    "wl_b6": {"B64_WL_BATCH": 6},
+    "wl_b7": {"B64_WL_BATCH": 7},
+    "wl_b5": {"B64_WL_BATCH": 5},
     "wr_b4": {"B64_WR_BATCH": 4},
     "wr_b2": {"B64_WR_BATCH": 2},
     "wr_b8": {"B64_WR_BATCH": 8},
