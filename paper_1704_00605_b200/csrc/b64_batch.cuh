@@ -578,16 +578,38 @@ __global__ void __launch_bounds__(kBThreads, 1)
   if constexpr (DECODE) {
     // ---- phase 3: per-message results.  After the grid sync every error
     // atomic has landed; status is a pure function of err_pos (R-length).
+    // A thread's first message is read before the barrier (its offsets and
+    // last four characters -- all finish_stream looks at), so after it only
+    // the error slot is loaded.
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kBThreads + tid;
+    int64_t pa = 0, pb = 0, po = 0;
+    uint32_t last4 = 0;
+    if (i0 < k) {
+      pa = in_off[i0];
+      pb = in_off[i0 + 1];
+      po = out_off[i0];
+      const int64_t base = pb - pa >= 4 ? pb - 4 : pa;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (base + j < pb) last4 |= static_cast<uint32_t>(in[base + j]) << (8 * j);
+    }
     __threadfence();
     grid.sync();
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kBThreads + tid; i < k;
-         i += static_cast<int64_t>(gridDim.x) * kBThreads) {
-      const int64_t a = in_off[i], b = in_off[i + 1];
+    for (int64_t i = i0; i < k; i += static_cast<int64_t>(gridDim.x) * kBThreads) {
+      const bool pre = i == i0;
+      const int64_t a = pre ? pa : in_off[i], b = pre ? pb : in_off[i + 1];
       const int64_t len = b - a;
       if (len / 4 == 0 && !((flags & kFlagNoPad) && len >= 2)) continue;  // decided in phase 1
       int64_t err = len / 4 == 0 ? LLONG_MAX : err_pos[i];
       if (err == LLONG_MAX) err = -1;
-      const StreamResult R = finish_stream(in + a, len, out + out_off[i], err, true, flags);
+      const uint8_t *c = in + a;
+      const int64_t cb = len >= 4 ? len - 4 : 0;  // index of last4's byte 0
+      const uint32_t l4 = last4;
+      const StreamResult R = finish_stream_at(
+          [pre, c, cb, l4](int64_t x) -> uint32_t {
+            return pre ? (l4 >> (8 * static_cast<uint32_t>(x - cb))) & 0xFFu : c[x];
+          },
+          len, out + (pre ? po : out_off[i]), err, true, flags);
       status[i] = R.status;
       out_len[i] = R.out_len;
       err_pos[i] = R.err_pos;
