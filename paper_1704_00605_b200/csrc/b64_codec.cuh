@@ -43,8 +43,8 @@ namespace b64 {
 #ifndef B64_ENC_ARITH  // measurement only: Table I mapping by SWAR arithmetic instead of the table
 #define B64_ENC_ARITH 0
 #endif
-#ifndef B64_DEC_STG32  // measurement only: decode DIRECT tiles store from registers
-#define B64_DEC_STG32 0
+#ifndef B64_DEC_STG32  // decode DIRECT tiles: three 4-byte stores from registers (no smem slice)
+#define B64_DEC_STG32 1
 #endif
 #ifndef B64_STORE_EVICT_FIRST
 #define B64_STORE_EVICT_FIRST 0
@@ -322,10 +322,13 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
 // warp __reduce_min_sync.  Returns (lane 0 meaningful) the tile-relative
 // minimum error offset, or 0xFFFFFFFF.
 // FULL: the tile has exactly DecG<P>::kIn chars and is not a final tile.
-// DIRECT (FULL tiles, 16-byte aligned destination): the warp stages its 384
-// output bytes of the pass in its own slice of smem (3 conflict-free STS per
-// lane), then lanes 0..23 copy them to HBM with coalesced 16-byte stores --
-// warp-local, no CTA-wide barrier, no bulk-store round trip.
+// DIRECT (FULL tiles, 16-byte aligned destination): each thread stores its
+// 12 bytes straight from registers with three 4-byte stores (B64_DEC_STG32,
+// the default: no shared-memory traffic for the output, which matters once
+// the power cap lowers the SM clock), or (B64_DEC_STG32=0) the warp stages
+// its 384 output bytes in its own slice of smem (3 conflict-free STS per
+// lane) and lanes 0..23 copy them with coalesced 16-byte stores.  Both are
+// warp-local: no CTA-wide barrier, no bulk-store round trip.
 template <int IA, int OA, bool FULL, int P, bool DIRECT = false, int NT = kNT>
 __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8_t *sout,
                                                 int tid, int lane,
@@ -405,7 +408,7 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
     o[1] = __byte_perm(V[1], V[2], 0x5601);
     o[2] = __byte_perm(V[2], V[3], 0x4560);
 #if B64_DEC_STG32
-    if constexpr (DIRECT) {  // measurement variant: three 4-byte stores straight from registers
+    if constexpr (DIRECT) {  // three 4-byte stores straight from registers (lanes 12 B apart)
       uint32_t *g = reinterpret_cast<uint32_t *>(gdst + bo);
       g[0] = o[0];
       g[1] = o[1];

@@ -71,6 +71,7 @@ VARIANTS = {
     "b_w20": {"B64_BATCH_WARPS": 20},
     "b_trace": {"B64_BATCH_TRACE": 1},
     "dec_stg32": {"B64_DEC_STG32": 1},
+    "dec_slice": {"B64_DEC_STG32": 0},
     "b_pf4": {"B64_BATCH_PREFETCH": 4},
     "wl_sleep0": {"B64_WL_SLEEP": 0},
     "wl_sleep64": {"B64_WL_SLEEP": 64},
