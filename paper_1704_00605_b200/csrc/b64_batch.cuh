@@ -10,7 +10,7 @@
 // takes an equal, contiguous range of units -- i.e. messages are assigned to
 // warps by prefix-summed lengths -- gets its first message from a table the
 // plan writes and walks forward.  Warps are fully independent: each owns a
-// 4-slot ring of 1-D TMA bulk loads (its lane 0 issues them, one mbarrier per
+// 2-slot ring of 1-D TMA bulk loads (its lane 0 issues them, one mbarrier per
 // slot), a private output slice in smem, and writes its unit's output with
 // coalesced 16-byte stores (byte stores for the <16-byte unaligned edges).
 // There is no CTA-wide barrier on the hot path.
@@ -304,7 +304,7 @@ __device__ __forceinline__ void warp_copy_out(uint8_t *gdst, const uint8_t *stre
 
 // --------------------------------------------------------- the kernel ---
 template <bool DECODE>
-__global__ void __launch_bounds__(kBThreads, 1)
+__global__ void __launch_bounds__(kBThreads, B64_BATCH_CTAS)
     batch_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t k,
                  const int64_t *__restrict__ in_off, int64_t *__restrict__ out_off,
                  int64_t *__restrict__ unit_off, int64_t *__restrict__ blk,

@@ -26,10 +26,13 @@ namespace b64 {
 #define B64_BATCH_PASSES 4
 #endif
 #ifndef B64_BATCH_SLOTS   // per-warp input ring depth (batched)
-#define B64_BATCH_SLOTS 4
+#define B64_BATCH_SLOTS 2
 #endif
 #ifndef B64_BATCH_PREFETCH  // batched: L2 prefetch distance in units (0 = off)
 #define B64_BATCH_PREFETCH 0
+#endif
+#ifndef B64_BATCH_CTAS    // batched: CTAs per SM of the cooperative grid
+#define B64_BATCH_CTAS 1
 #endif
 #ifndef B64_BATCH_WARPS   // warps per CTA (batched)
 #define B64_BATCH_WARPS 16

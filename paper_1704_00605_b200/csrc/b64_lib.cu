@@ -584,7 +584,8 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
                : B64_ERR_CUDA;
   }
   // One cooperative launch: plan + grid sync + codec (all CTAs co-resident).
-  const unsigned grid = static_cast<unsigned>(sms < kMaxBatchCtas ? sms : kMaxBatchCtas);
+  const int bg = sms * B64_BATCH_CTAS;
+  const unsigned grid = static_cast<unsigned>(bg < kMaxBatchCtas ? bg : kMaxBatchCtas);
   const uint8_t *a_in = d_in;
   uint8_t *a_out = d_out;
   int64_t a_k = k;
