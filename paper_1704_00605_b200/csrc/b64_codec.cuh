@@ -332,11 +332,13 @@ __device__ __forceinline__ void encode_tile(const uint8_t *sin, int L, uint8_t *
 // its 384 output bytes in its own slice of smem (3 conflict-free STS per
 // lane) and lanes 0..23 copy them with coalesced 16-byte stores.  Both are
 // warp-local: no CTA-wide barrier, no bulk-store round trip.
+// DIRECT with !FULL (B64_DEC_STG32; 4-byte aligned gdst): the tile's output
+// is its first olim bytes (3 L / 4 minus the final quad's pads).
 template <int IA, int OA, bool FULL, int P, bool DIRECT = false, int NT = kNT>
 __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8_t *sout,
                                                 int tid, int lane,
                                                 bool final_tile, uint32_t ch2, uint32_t ch1,
-                                                uint8_t *gdst = nullptr) {
+                                                uint8_t *gdst = nullptr, int olim = 0) {
   uint32_t errmin = 0xFFFFFFFFu;
   const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(g_dec_tab));
 #pragma unroll
@@ -412,10 +414,17 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
     o[2] = __byte_perm(V[2], V[3], 0x4560);
 #if B64_DEC_STG32
     if constexpr (DIRECT) {  // three 4-byte stores straight from registers (lanes 12 B apart)
-      uint32_t *g = reinterpret_cast<uint32_t *>(gdst + bo);
-      g[0] = o[0];
-      g[1] = o[1];
-      g[2] = o[2];
+      if (FULL || (active && bo + 12 <= olim)) {
+        uint32_t *g = reinterpret_cast<uint32_t *>(gdst + bo);
+        g[0] = o[0];
+        g[1] = o[1];
+        g[2] = o[2];
+      } else if (active) {  // the run holding the stream's padded final quad: its olim - bo bytes
+        for (int j = 0; j < olim - bo; ++j) {
+          const uint32_t w = j < 4 ? o[0] : j < 8 ? o[1] : o[2];
+          gdst[bo + j] = static_cast<uint8_t>(w >> (8 * (j & 3)));
+        }
+      }
       continue;
     }
 #endif

@@ -28,6 +28,10 @@
 #include "b64_compact.cuh"
 #include "b64_ptx.cuh"
 
+#ifndef B64_WS_DIRECT  // general path: decode runs store from registers (4-byte aligned output)
+#define B64_WS_DIRECT 1
+#endif
+
 namespace b64 {
 
 // Per-call scratch (device, caller workspace): errkey / done are reset by the
@@ -65,6 +69,11 @@ __device__ __forceinline__ uint32_t ws_decode_run(WsSmem &S, const uint8_t *sin,
   const int mis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
   constexpr int P = (kCpTile + 16) / (kCpThreads * 16) + 1;  // passes of 512 x 16 chars
   uint32_t e;
+#if B64_DEC_STG32 && B64_WS_DIRECT
+  if ((mis & 3) == 0)  // each thread's 12 bytes straight to HBM: no staging, no barrier
+    return decode_tile<16, 4, false, P, true, kCpThreads>(sin, n, nullptr, tid, lane, fin, ch2,
+                                                          ch1, gdst, olen);
+#endif
   if ((mis & 3) == 0)
     e = decode_tile<16, 4, false, P, false, kCpThreads>(sin, n, S.ostage + mis, tid, lane, fin,
                                                         ch2, ch1);
