@@ -317,7 +317,11 @@ __device__ __forceinline__ void cta_copy_out_congruent(uint8_t *dst, const uint8
 #ifndef B64_DS_GROUP
 #define B64_DS_GROUP 1
 #endif
+#ifndef B64_DS_DEFER  // copy tile t's stream out after tile t+1's compaction barrier
+#define B64_DS_DEFER 1
+#endif
 constexpr int kDsGroup = B64_DS_GROUP;  // tiles compacted per copy-out
+static_assert(!B64_DS_DEFER || B64_DS_GROUP == 1, "B64_DS_DEFER needs B64_DS_GROUP 1");
 constexpr int kDsStages = kCpStages + kDsGroup - 1;
 
 struct alignas(128) DsSmem {
@@ -326,7 +330,11 @@ struct alignas(128) DsSmem {
   uint64_t full[kDsStages];
   int32_t wcnt[2][kCpWarps];
   uint32_t ktab[16];
+#if B64_DS_DEFER
+  alignas(16) uint8_t stream[2][kCpTile + 32];  // tile t's stream is copied out during tile t+1
+#else
   alignas(16) uint8_t stream[kDsGroup * kCpTile + 32];  // 16-aligned: LDS.128 copy-out
+#endif
   int64_t red[66];
 };
 
@@ -361,6 +369,33 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
   if (tid == 0)
     for (int s = 0; s < kDsStages - 1 && t0 + s < t1; ++s) load(t0 + s, s);
   const uintptr_t obase = reinterpret_cast<uintptr_t>(out);
+#if B64_DS_DEFER
+  // Double-buffered streams: compact_tile(t+1)'s internal barrier already
+  // orders every thread's placement stores of tile t before the copy-out of
+  // tile t, so the copy-out needs no barrier of its own and overlaps the
+  // next tile's compaction across warps.
+  int64_t prun = 0;
+  int pdst = 0, pn = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int it = static_cast<int>(t - t0);
+    const int s = it % kDsStages, b = it & 1;
+    const int dst = static_cast<int>((obase + static_cast<uintptr_t>(running)) & 15);
+    ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kDsStages) & 1));
+    const int n = compact_tile(S.win[s], S.msk[s], S.stream[b], dst, S.wcnt[b], S.ktab);
+    ptx::fence_proxy_async_smem();  // generic reads of win[s] before its next bulk write
+    if (tid == 0 && t + kDsStages - 1 < t1)
+      load(t + kDsStages - 1, static_cast<int>((it + kDsStages - 1) % kDsStages));
+    if (it > 0) cta_copy_out_congruent(out + prun, S.stream[b ^ 1] + pdst, pn);
+    prun = running;
+    pdst = dst;
+    pn = n;
+    running += n;
+  }
+  if (t1 > t0) {
+    __syncthreads();
+    cta_copy_out_congruent(out + prun, S.stream[(t1 - 1 - t0) & 1] + pdst, pn);
+  }
+#else
   int64_t t = t0;
   while (t < t1) {
     // kDsGroup tiles compacted back to back into one stream, one copy-out:
@@ -383,6 +418,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     cta_copy_out_congruent(out + running, S.stream + dst, n);
     running += n;
   }
+#endif
   if (blockIdx.x == gridDim.x - 1 && tid == 0) *out_len = total;
 }
 

@@ -72,6 +72,7 @@ VARIANTS = {
     "b_trace": {"B64_BATCH_TRACE": 1},
     "dec_stg32": {"B64_DEC_STG32": 1},
     "dec_slice": {"B64_DEC_STG32": 0},
+    "ds_nodefer": {"B64_DS_DEFER": 0},
     "ws_nodirect": {"B64_WS_DIRECT": 0},
     "b_c2_s2": {"B64_BATCH_CTAS": 2, "B64_BATCH_SLOTS": 2},
     "b_c2_s2_w8": {"B64_BATCH_CTAS": 2, "B64_BATCH_SLOTS": 3, "B64_BATCH_WARPS": 8},
