@@ -7,6 +7,8 @@ space, random line geometry.  Every case compares output bytes, lengths,
 status and error offset exactly; output guard bytes must stay untouched.
 The cases are drawn from numpy generators with fixed seeds, so a failure
 names a reproducible (seed, case)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -21,6 +23,10 @@ pytestmark = pytest.mark.gpu
 U, NP, ST = b64.B64_FLAG_URL, b64.B64_FLAG_NOPAD, b64.B64_FLAG_STRICT
 FLAGS = [0, U, NP, ST, U | NP, NP | ST, U | ST, U | NP | ST]
 WS = np.frombuffer(b" \n\r", dtype=np.uint8)
+# B64_FUZZ_SCALE multiplies every case count, B64_FUZZ_SEED shifts every
+# seed (longer one-off runs; the defaults are the committed suite).
+SCALE = int(os.environ.get("B64_FUZZ_SCALE", "1"))
+SEED = int(os.environ.get("B64_FUZZ_SEED", "0"))
 NA = np.array([b for b in range(256) if b not in b"=" and oracle.A(b) < 0 and oracle.A_ex(b, U) < 0
                and b not in b" \n\r"], dtype=np.uint8)
 
@@ -70,8 +76,8 @@ def corrupt(rng, t, fl):
 
 
 def test_fuzz_single_buffer():
-    rng = np.random.default_rng(9001)
-    for case in range(400):
+    rng = np.random.default_rng(9001 + SEED)
+    for case in range(400 * SCALE):
         n = rand_len(rng)
         fl = FLAGS[int(rng.integers(0, len(FLAGS)))]
         im, om = int(rng.integers(0, 16)), int(rng.integers(0, 16))
@@ -97,8 +103,8 @@ def test_fuzz_single_buffer():
 
 
 def test_fuzz_batched():
-    rng = np.random.default_rng(9002)
-    for case in range(60):
+    rng = np.random.default_rng(9002 + SEED)
+    for case in range(60 * SCALE):
         k = int(rng.integers(0, 400))
         mode = case % 3
         if mode == 0:
@@ -143,8 +149,8 @@ def sprinkle(rng, t, frac):
 
 
 def test_fuzz_whitespace_and_lines():
-    rng = np.random.default_rng(9003)
-    for case in range(200):
+    rng = np.random.default_rng(9003 + SEED)
+    for case in range(200 * SCALE):
         n = rand_len(rng, 400_000)
         fl = FLAGS[int(rng.integers(0, len(FLAGS)))]
         x = splitmix_bytes(9003, case * 5_000_011, case * 5_000_011 + n)
@@ -190,8 +196,8 @@ def test_fuzz_shards():
     combine (min error offset, summed lengths) to the whole-buffer decode."""
     from paper_1704_00605_b200.dist import INT64_MAX, global_decode_result
 
-    rng = np.random.default_rng(9004)
-    for case in range(40):
+    rng = np.random.default_rng(9004 + SEED)
+    for case in range(40 * SCALE):
         n = rand_len(rng, 500_000)
         world = int(rng.integers(1, 9))
         x = splitmix_bytes(9004, case * 3_000_017, case * 3_000_017 + n)
@@ -223,8 +229,8 @@ def test_fuzz_shards():
 def test_fuzz_host_buffers():
     """The host-buffer pipeline (copies inside the call) on random sizes,
     pinned and pageable host memory, clean and corrupted text."""
-    rng = np.random.default_rng(9005)
-    for case in range(20):
+    rng = np.random.default_rng(9005 + SEED)
+    for case in range(20 * SCALE):
         n = rand_len(rng, 3_000_000)
         x = splitmix_bytes(9005, case * 4_000_037, case * 4_000_037 + n)
         pin = bool(rng.integers(0, 2))
