@@ -200,7 +200,7 @@ struct alignas(128) CpSmem {
   uint8_t win[kCpStages][kCpTile];         // TMA ring (16-byte aligned windows)
   uint32_t msk[kCpStages][kCpThreads];     // the tiles' keep masks (cp_mask_kernel)
   uint64_t full[kCpStages];
-  int32_t wcnt[kCpWarps];
+  int32_t wcnt[2][kCpWarps];  // by tile parity: back-to-back compactions need no extra barrier
   uint32_t ktab[16];  // per 4-bit keep mask: PRMT selector (bits 0..15) | (2^c - 1) << 16
 };
 

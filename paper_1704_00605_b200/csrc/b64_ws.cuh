@@ -191,28 +191,13 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     for (int s = 0; s < kCpStages - 1 && t0 + s < t1; ++s) cp_load(S.cp, G, masks, t0 + s, s, pol);
 
   const int64_t own0 = (Pb + 15) & ~static_cast<int64_t>(15);  // first block this chunk owns
-  int64_t Q = Pb, Bprev = Pb & ~static_cast<int64_t>(15);
-  for (int64_t t = t0; t < t1; ++t) {
-    const int it = static_cast<int>(t - t0);
-    const int s = it % kCpStages, sb = it & 1;
-    if (tid == 0 && t + kCpStages - 1 < t1)
-      cp_load(S.cp, G, masks, t + kCpStages - 1, (it + kCpStages - 1) % kCpStages, pol);
-    const int64_t Bc = Q & ~static_cast<int64_t>(15);
-    const int dst = static_cast<int>(Q & 15);
-    // carry: the characters [Bc, Q) of an incomplete block, from the previous stream
-    if (tid == 0 && dst != 0 && it > 0)
-      *reinterpret_cast<uint4 *>(S.stream[sb]) =
-          *reinterpret_cast<const uint4 *>(S.stream[sb ^ 1] + (Bc - Bprev));
-    ptx::mbar_wait_spin(&S.cp.full[s], static_cast<uint32_t>((it / kCpStages) & 1));
-    const int n = compact_tile(S.cp.win[s], S.cp.msk[s], S.stream[sb], dst, S.cp.wcnt, S.cp.ktab);
-    ptx::fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) tcnt[t] = n;
-    const int64_t Qn = Q + n;
-    const int64_t d0 = Bc > own0 ? Bc : own0;
-    const int64_t d1 = Qn & ~static_cast<int64_t>(15);
+  // Decode the full 16-char blocks [d0, d1) of a tile's compacted stream
+  // (stream base Bc_ at compact position Bc_), reporting its first error.
+  auto decode_blocks = [&](const uint8_t *stream, int64_t Bc_, int64_t Qn_) {
+    const int64_t d0 = Bc_ > own0 ? Bc_ : own0;
+    const int64_t d1 = Qn_ & ~static_cast<int64_t>(15);
     if (d1 > d0) {  // full blocks [d0, d1); warp-uniform
-      const uint8_t *sin = S.stream[sb] + (d0 - Bc);
+      const uint8_t *sin = stream + (d0 - Bc_);
       const int nc = static_cast<int>(d1 - d0);
       const bool fin = d1 == M;  // the stream ends on this block boundary (M % 16 == 0)
       uint32_t ch2 = 0, ch1 = 0;
@@ -232,8 +217,36 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
           atomicMin(&hdr->errkey, pos);
       }
     }
-    Q = Qn;
+  };
+  // Tile t is decoded during iteration t+1, after tile t+1's compaction
+  // barrier (which orders every thread's placement stores of tile t): one
+  // CTA barrier per tile.  The carry of an incomplete block into tile t+1's
+  // stream ([0, dst) of it: disjoint from tile t+1's own bytes) is copied
+  // after that barrier too.
+  int64_t Q = Pb, Bprev = Pb & ~static_cast<int64_t>(15);
+  int64_t pBc = 0, pQn = 0;  // the pending (compacted, not yet decoded) tile
+  for (int64_t t = t0; t < t1; ++t) {
+    const int it = static_cast<int>(t - t0);
+    const int s = it % kCpStages, sb = it & 1;
+    const int64_t Bc = Q & ~static_cast<int64_t>(15);
+    const int dst = static_cast<int>(Q & 15);
+    ptx::mbar_wait_spin(&S.cp.full[s], static_cast<uint32_t>((it / kCpStages) & 1));
+    const int n = compact_tile(S.cp.win[s], S.cp.msk[s], S.stream[sb], dst, S.cp.wcnt[sb], S.cp.ktab);
+    ptx::fence_proxy_async_smem();
+    // the previous tile's window and stream are complete / free now
+    if (tid == 0 && t + kCpStages - 1 < t1)
+      cp_load(S.cp, G, masks, t + kCpStages - 1, (it + kCpStages - 1) % kCpStages, pol);
+    if (it > 0 && tid < dst) S.stream[sb][tid] = S.stream[sb ^ 1][Bc - Bprev + tid];
+    if (tid == 0) tcnt[t] = n;
+    if (it > 0) decode_blocks(S.stream[sb ^ 1], pBc, pQn);
+    pBc = Bc;
+    pQn = Q + n;
+    Q = pQn;
     Bprev = Bc;
+  }
+  if (t1 > t0) {
+    __syncthreads();  // the last tile's placement stores and carry
+    decode_blocks(S.stream[(t1 - 1 - t0) & 1], pBc, pQn);
   }
 
   // Boundary block: [sblk, sblk + 16) straddles the chunk's end (or is the
