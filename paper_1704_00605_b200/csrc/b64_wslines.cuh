@@ -178,7 +178,10 @@ __global__ void __launch_bounds__(kWlThreads, 2)
         const int s = k % kWlStages;
         ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((k / kWlStages) & 1));
         int stop = 0;
-        if (lane == 0) stop = S.flag | *reinterpret_cast<volatile int32_t *>(&st->viol);
+        // another CTA's violation only needs to stop this one eventually (the
+        // verdict is decided at the end): poll the global flag every 8th tile
+        if (lane == 0)
+          stop = S.flag | ((k & 7) == 7 ? *reinterpret_cast<volatile int32_t *>(&st->viol) : 0);
         stop = __shfl_sync(0xffffffffu, stop, 0);
         if (!stop) {
           const int64_t src = t * Lt * static_cast<int64_t>(Sl);
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kWlThreads, 2)
             }
           }
           // EOL of every line whose last quad this warp owns (and that has one)
-          for (int ln = qa / G + lane; ln < qb / G; ln += 32) {
+          for (int ln = line_of(qa) + lane, lb = line_of(qb); ln < lb; ln += 32) {
             if ((line0 + ln + 1) * Sl > M) break;
             const int b = imis + ln * Sl + L;
             const uint32_t x = __funnelshift_r(win[b >> 2], win[(b >> 2) + 1], 8 * (b & 3));
