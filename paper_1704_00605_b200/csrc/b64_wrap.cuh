@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kWrThreads, 2)
     if (tid == 0 && t + (kWrStages - 1) * static_cast<int64_t>(gridDim.x) < ntiles)
       load(t + (kWrStages - 1) * static_cast<int64_t>(gridDim.x), (it + kWrStages - 1) % kWrStages);
     const int64_t src = t * tin, dst = t * tout;
-    const int64_t g0 = src / 3;  // first group of the tile
+    const int64_t g0 = t * static_cast<int64_t>(W.Lt) * W.G;  // first group of the tile (= src / 3)
     const int64_t gend = (g0 + static_cast<int64_t>(W.Lt) * W.G) < W.ng
                              ? g0 + static_cast<int64_t>(W.Lt) * W.G : W.ng;
     const int ngrp = static_cast<int>(gend - g0);
