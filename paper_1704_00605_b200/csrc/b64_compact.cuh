@@ -233,6 +233,11 @@ __device__ __forceinline__ void cp_load(CpSmem &S, const CpGeom &G, const uint32
 // masks msk[tid] from cp_mask_kernel) into stream[dst, dst + n), in order;
 // returns n (all threads).  Contains one __syncthreads; the caller
 // synchronises before reading the stream.
+// PIPE: word i+1 and its selector are loaded before word i's byte stores
+// (the compiler keeps shared loads below earlier shared stores otherwise,
+// which puts a load latency on every word) -- measured faster in the fused
+// decode (1.068 -> 1.057 ms), marginally slower in despace (0.811 vs 0.816).
+template <bool PIPE>
 __device__ __forceinline__ int compact_tile(const uint8_t *win, const uint32_t *msk,
                                             uint8_t *stream, int dst, int32_t *wcnt,
                                             const uint32_t *ktab) {
@@ -273,12 +278,28 @@ __device__ __forceinline__ int compact_tile(const uint8_t *win, const uint32_t *
   const int total = __shfl_sync(0xffffffffu, incl, kCpWarps - 1);
   uint8_t *ws = stream + dst + wpre;
   int base = 0;  // kept bytes of this warp's words 32*i' + *, i' < i
+  uint32_t en = 0, wn = 0;
+  if constexpr (PIPE) {
+    en = ktab[nib & 0xFu];
+    wn = seg[0];
+  }
 #pragma unroll
   for (int i = 0; i < kCpPerLane; ++i) {
     // the word's kept bytes, packed low by one PRMT, stored at p[0..c)
-    const uint32_t e = ktab[(nib >> (4 * i)) & 0xFu];
+    uint32_t e, wsrc;
+    if constexpr (PIPE) {
+      e = en;
+      wsrc = wn;
+      if (i + 1 < kCpPerLane) {
+        en = ktab[(nib >> (4 * (i + 1))) & 0xFu];
+        wn = seg[32 * (i + 1)];
+      }
+    } else {
+      e = ktab[(nib >> (4 * i)) & 0xFu];
+      wsrc = seg[32 * i];
+    }
     uint32_t cw;  // PRMT reads only the selector's low 16 bits
-    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(cw) : "r"(seg[32 * i]), "r"(e));
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(cw) : "r"(wsrc), "r"(e));
     const uint32_t E = (i & 1) ? e1 : e0, T = (i & 1) ? T1 : T0;
     const int sh = 8 * (i >> 1);
     uint8_t *p = ws + base + static_cast<int>((E >> sh) & 0xFFu);
@@ -381,7 +402,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     const int s = it % kDsStages, b = it & 1;
     const int dst = static_cast<int>((obase + static_cast<uintptr_t>(running)) & 15);
     ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kDsStages) & 1));
-    const int n = compact_tile(S.win[s], S.msk[s], S.stream[b], dst, S.wcnt[b], S.ktab);
+    const int n = compact_tile<false>(S.win[s], S.msk[s], S.stream[b], dst, S.wcnt[b], S.ktab);
     ptx::fence_proxy_async_smem();  // generic reads of win[s] before its next bulk write
     if (tid == 0 && t + kDsStages - 1 < t1)
       load(t + kDsStages - 1, static_cast<int>((it + kDsStages - 1) % kDsStages));
@@ -408,7 +429,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
       const int it = static_cast<int>(t - t0);
       const int s = it % kDsStages;
       ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kDsStages) & 1));
-      n += compact_tile(S.win[s], S.msk[s], S.stream, dst + n, S.wcnt[j & 1], S.ktab);
+      n += compact_tile<false>(S.win[s], S.msk[s], S.stream, dst + n, S.wcnt[j & 1], S.ktab);
       ptx::fence_proxy_async_smem();  // generic reads of win[s] before its next bulk write
       // slot of tile t-1 is free (all warps passed this tile's internal barrier)
       if (tid == 0 && t + kDsStages - 1 < t1)

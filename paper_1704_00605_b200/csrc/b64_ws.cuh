@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     const int64_t Bc = Q & ~static_cast<int64_t>(15);
     const int dst = static_cast<int>(Q & 15);
     ptx::mbar_wait_spin(&S.cp.full[s], static_cast<uint32_t>((it / kCpStages) & 1));
-    const int n = compact_tile(S.cp.win[s], S.cp.msk[s], S.stream[sb], dst, S.cp.wcnt[sb], S.cp.ktab);
+    const int n = compact_tile<true>(S.cp.win[s], S.cp.msk[s], S.stream[sb], dst, S.cp.wcnt[sb], S.cp.ktab);
     ptx::fence_proxy_async_smem();
     // the previous tile's window and stream are complete / free now
     if (tid == 0 && t + kCpStages - 1 < t1)
