@@ -46,6 +46,15 @@ using EncS1 = EncG<kSinglePasses>;  // single-buffer tile geometry
 using DecS1 = DecG<kSinglePasses>;
 using EncSmem = Smem<EncS1::kIn, EncS1::kOut>;
 using DecSmem = Smem<DecS1::kIn, DecS1::kOut>;
+// Small inputs (fewer tiles than ~2 per SM at the default geometry) use
+// half-size tiles so that twice as many SMs work on them: the call is
+// latency-bound there (BASELINE config 1, 1 MiB), bandwidth-bound above.
+#ifndef B64_SMALL_PASSES
+#define B64_SMALL_PASSES 2
+#endif
+constexpr int kSmallPasses = B64_SMALL_PASSES;
+template <int P> using EncSmemP = Smem<EncG<P>::kIn, EncG<P>::kOut>;
+template <int P> using DecSmemP = Smem<DecG<P>::kIn, DecG<P>::kOut>;
 
 struct DecWs {                 // per-(device, stream) decode scratch (self-resetting)
   unsigned long long errkey;   // min error offset, ~0 = none
@@ -54,27 +63,31 @@ struct DecWs {                 // per-(device, stream) decode scratch (self-rese
 };
 
 // ------------------------------------------------- tile descriptors ---
+template <int P>
 __device__ __forceinline__ TileDesc enc_single_desc(int64_t j, int64_t n) {
+  using GE = EncG<P>;
   TileDesc d;
-  d.src = j * EncS1::kIn;
-  d.dst = j * EncS1::kOut;
+  d.src = j * GE::kIn;
+  d.dst = j * GE::kOut;
   d.rel = d.src;
   const int64_t left = n - d.src;
-  d.len = static_cast<int32_t>(left < EncS1::kIn ? left : EncS1::kIn);
+  d.len = static_cast<int32_t>(left < GE::kIn ? left : GE::kIn);
   d.msg = 0;
   d.flags = 0;
   d.ntiles = 0;
   return d;
 }
 
+template <int P>
 __device__ __forceinline__ TileDesc dec_single_desc(int64_t j, int64_t ntiles, int64_t chars,
                                                     bool final_pad_rules) {
+  using GD = DecG<P>;
   TileDesc d;
-  d.src = j * DecS1::kIn;
-  d.dst = j * DecS1::kOut;
+  d.src = j * GD::kIn;
+  d.dst = j * GD::kOut;
   d.rel = d.src;
   const int64_t left = chars - d.src;
-  d.len = static_cast<int32_t>(left < DecS1::kIn ? left : DecS1::kIn);
+  d.len = static_cast<int32_t>(left < GD::kIn ? left : GD::kIn);
   d.msg = 0;
   d.flags = (final_pad_rules && j == ntiles - 1) ? kFlagFinal : 0;
   d.ntiles = 0;
@@ -85,15 +98,15 @@ __device__ __forceinline__ TileDesc dec_single_desc(int64_t j, int64_t ntiles, i
 // Lane 0 owns the ring: wait for the slot, publish the descriptor, arm the
 // full barrier with the byte count and issue the bulk copy of the tile's
 // 16-byte aligned window (evict-first: the input is streamed once).
-template <bool DECODE, class SmemT>
+template <bool DECODE, int P, class SmemT>
 __device__ __forceinline__ void producer_loop(SmemT &S, const uint8_t *in, int64_t ntiles,
                                               int64_t n_or_chars, bool final_pad_rules, int lane) {
   if (lane != 0) return;
   const uint64_t pol = policy_evict_first();
   int it = 0;
   for (int64_t j = blockIdx.x; j < ntiles; j += gridDim.x, ++it) {
-    const TileDesc d = DECODE ? dec_single_desc(j, ntiles, n_or_chars, final_pad_rules)
-                              : enc_single_desc(j, n_or_chars);
+    const TileDesc d = DECODE ? dec_single_desc<P>(j, ntiles, n_or_chars, final_pad_rules)
+                              : enc_single_desc<P>(j, n_or_chars);
     const int s = it % kStagesIn;
     if (it >= kStagesIn) mbar_wait(&S.empty[s], ((it / kStagesIn) & 1) ^ 1);
     S.desc[s] = d;
@@ -135,13 +148,13 @@ __device__ __forceinline__ void copy_out(uint8_t *gdst, const uint8_t *sbuf, int
 // ------------------------------------------------------ encode kernel ---
 // Single buffer (rows a1-a5).  IA / OA: guaranteed alignment class of the
 // input / output pointer (16, 4 or 1).
-template <int IA, int OA>
+template <int IA, int OA, int P = kSinglePasses>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     encode_kernel(const uint8_t *__restrict__ in, int64_t n, uint8_t *__restrict__ out,
                   int64_t ntiles, int flags) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using G = EncS1;
-  EncSmem &S = *reinterpret_cast<EncSmem *>(smem_raw);
+  using G = EncG<P>;
+  EncSmemP<P> &S = *reinterpret_cast<EncSmemP<P> *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < 64) g_enc_tab[tid] = static_cast<uint8_t>(ascii_of(tid, flags));  // Table I / II
   const bool pad = !(flags & kFlagNoPad);
@@ -155,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   __syncthreads();
 
   if (warp == kWarpsC) {
-    producer_loop<false>(S, in, ntiles, n, false, lane);
+    producer_loop<false, P>(S, in, ntiles, n, false, lane);
     return;
   }
 
@@ -193,13 +206,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
 // ------------------------------------------------------ decode kernel ---
 // Single buffer / shard (rows a6-a12).
-template <int IA, int OA>
+template <int IA, int OA, int P = kSinglePasses>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
                   int64_t ntiles, int final_shard, DecWs *ws, b64_result *res, int flags) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using G = DecS1;
-  DecSmem &S = *reinterpret_cast<DecSmem *>(smem_raw);
+  using G = DecG<P>;
+  DecSmemP<P> &S = *reinterpret_cast<DecSmemP<P> *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t chars = 4 * (m / 4);
   const bool pad_rules = final_shard != 0 && (m % 4) == 0;
@@ -218,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   __syncthreads();
 
   if (warp == kWarpsC) {
-    producer_loop<true>(S, in, ntiles, chars, pad_rules, lane);
+    producer_loop<true, P>(S, in, ntiles, chars, pad_rules, lane);
     return;
   }
 
@@ -344,6 +357,17 @@ DecFn dec_table[3][3] = {
     {decode_kernel<4, 16>, decode_kernel<4, 4>, decode_kernel<4, 1>},
     {decode_kernel<1, 16>, decode_kernel<1, 4>, decode_kernel<1, 1>},
 };
+constexpr int SP = kSmallPasses;
+EncFn enc_small_table[3][3] = {
+    {encode_kernel<16, 16, SP>, encode_kernel<16, 4, SP>, encode_kernel<16, 1, SP>},
+    {encode_kernel<4, 16, SP>, encode_kernel<4, 4, SP>, encode_kernel<4, 1, SP>},
+    {encode_kernel<1, 16, SP>, encode_kernel<1, 4, SP>, encode_kernel<1, 1, SP>},
+};
+DecFn dec_small_table[3][3] = {
+    {decode_kernel<16, 16, SP>, decode_kernel<16, 4, SP>, decode_kernel<16, 1, SP>},
+    {decode_kernel<4, 16, SP>, decode_kernel<4, 4, SP>, decode_kernel<4, 1, SP>},
+    {decode_kernel<1, 16, SP>, decode_kernel<1, 4, SP>, decode_kernel<1, 1, SP>},
+};
 constexpr size_t kEncRingBytes = sizeof(EncRing) * kBWarps;
 constexpr size_t kDecRingBytes = sizeof(DecRing) * kBWarps;
 
@@ -367,6 +391,12 @@ bool device_setup(int *dev_out, int *sms_out) {
     for (auto &row : dec_table)
       for (auto f : row)
         if (set_smem(f, sizeof(DecSmem)) != cudaSuccess) return false;
+    for (auto &row : enc_small_table)
+      for (auto f : row)
+        if (set_smem(f, sizeof(EncSmemP<kSmallPasses>)) != cudaSuccess) return false;
+    for (auto &row : dec_small_table)
+      for (auto f : row)
+        if (set_smem(f, sizeof(DecSmemP<kSmallPasses>)) != cudaSuccess) return false;
     if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return false;
     if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return false;
     if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return false;
@@ -432,12 +462,14 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   const int64_t chars = 4 * (m / 4);
-  const int64_t ntiles = (chars + DecS1::kIn - 1) / DecS1::kIn;
+  int64_t ntiles = (chars + DecS1::kIn - 1) / DecS1::kIn;
+  const bool small = kSmallPasses != kSinglePasses && ntiles < 2 * static_cast<int64_t>(sms);
+  if (small) ntiles = (chars + DecG<kSmallPasses>::kIn - 1) / DecG<kSmallPasses>::kIn;
   const int64_t grid = grid_for(ntiles, sms);
-  DecFn f = dec_table[align_class(d_in)][align_class(d_out)];
-  f<<<static_cast<unsigned>(grid), kThreads, sizeof(DecSmem), stream>>>(d_in, m, d_out, ntiles,
-                                                                        final_shard, ws, d_result,
-                                                                        flags);
+  DecFn f = (small ? dec_small_table : dec_table)[align_class(d_in)][align_class(d_out)];
+  const size_t smem = small ? sizeof(DecSmemP<kSmallPasses>) : sizeof(DecSmem);
+  f<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(d_in, m, d_out, ntiles, final_shard, ws,
+                                                             d_result, flags);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
@@ -484,11 +516,13 @@ int64_t b64_encode_ex(const uint8_t *d_in, int64_t n, uint8_t *d_out, int flags,
   if (n == 0) return 0;
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
-  const int64_t ntiles = (n + EncS1::kIn - 1) / EncS1::kIn;
+  int64_t ntiles = (n + EncS1::kIn - 1) / EncS1::kIn;
+  const bool small = kSmallPasses != kSinglePasses && ntiles < 2 * static_cast<int64_t>(sms);
+  if (small) ntiles = (n + EncG<kSmallPasses>::kIn - 1) / EncG<kSmallPasses>::kIn;
   const int64_t grid = grid_for(ntiles, sms);
-  EncFn f = enc_table[align_class(d_in)][align_class(d_out)];
-  f<<<static_cast<unsigned>(grid), kThreads, sizeof(EncSmem), stream>>>(d_in, n, d_out, ntiles,
-                                                                          flags);
+  EncFn f = (small ? enc_small_table : enc_table)[align_class(d_in)][align_class(d_out)];
+  const size_t smem = small ? sizeof(EncSmemP<kSmallPasses>) : sizeof(EncSmem);
+  f<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(d_in, n, d_out, ntiles, flags);
   if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
   return enc_len(n, flags);
 }

@@ -17,8 +17,12 @@ from tests.gpu_util import DEV, empty_dev, host, to_dev
 pytestmark = pytest.mark.gpu
 
 ALPHABET = (string.ascii_uppercase + string.ascii_lowercase + string.digits + "+/").encode()
-ENC_TILE = 12288     # input bytes per single-buffer encode tile (EncG<kSinglePasses>::kIn)
-DEC_TILE = 16384     # input chars per single-buffer decode tile (DecG<kSinglePasses>::kIn)
+# Single-buffer tile geometry (b64_codec.cuh EncG / DecG, 512 compute threads):
+# the default 4 passes per tile, and 2 passes for inputs with fewer than 2
+# default tiles per SM (b64_lib.cu kSmallPasses).
+ENC_TILE, ENC_TILE_SMALL = 24576, 12288    # input bytes per encode tile
+DEC_TILE, DEC_TILE_SMALL = 32768, 16384    # input chars per decode tile
+SMALL_LIMIT = 2 * 148                      # default tiles below which the small geometry runs
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -65,9 +69,15 @@ def test_encode_every_length_0_to_1024():
         assert np.array_equal(gpu_encode(x[:n]), oracle.encode(x[:n])), n
 
 
-@pytest.mark.parametrize("tiles", [1, 2, 3, 295, 296, 297, 296 * 4 + 1, 296 * 9 + 7])
-def test_encode_tile_ring_boundaries(tiles):
-    base = tiles * ENC_TILE
+# (tile size, tile count): small-geometry boundaries below the switch,
+# default-geometry boundaries above it, and both sides of the switch itself
+ENC_CASES = [(ENC_TILE_SMALL, t) for t in (1, 2, 3, 295, 296, 297)] + \
+    [(ENC_TILE, t) for t in (SMALL_LIMIT - 1, SMALL_LIMIT, SMALL_LIMIT + 1, 296 * 4 + 1, 296 * 9 + 7)]
+
+
+@pytest.mark.parametrize("tile,tiles", ENC_CASES)
+def test_encode_tile_ring_boundaries(tile, tiles):
+    base = tiles * tile
     x = splitmix_bytes(102, 0, base + 4)
     for d in (-3, -2, -1, 0, 1, 2, 3, 4):
         n = base + d
@@ -119,9 +129,13 @@ def test_decode_length_errors():
     check_decode(u)
 
 
-@pytest.mark.parametrize("tiles", [1, 2, 295, 296, 297, 296 * 5 + 3])
-def test_decode_tile_ring_boundaries(tiles):
-    m0 = tiles * DEC_TILE
+DEC_CASES = [(DEC_TILE_SMALL, t) for t in (1, 2, 295, 296, 297)] + \
+    [(DEC_TILE, t) for t in (SMALL_LIMIT - 1, SMALL_LIMIT, SMALL_LIMIT + 1, 296 * 5 + 3)]
+
+
+@pytest.mark.parametrize("tile,tiles", DEC_CASES)
+def test_decode_tile_ring_boundaries(tile, tiles):
+    m0 = tiles * tile
     x = splitmix_bytes(106, 0, 3 * (m0 // 4) + 12)
     t = oracle.encode(x)
     for d in (-8, -4, 0, 4, 8):
@@ -143,8 +157,8 @@ def test_decode_all_misalignments():
 def test_decode_every_byte_at_every_position_of_a_block():
     """All 256 byte values at each position of a 64-char block in the middle
     of a 3-tile buffer, at the 16-char thread seams and the tile seam."""
-    x = splitmix_bytes(108, 0, 3 * DEC_TILE)
-    t = oracle.encode(x)          # 4 * DEC_TILE chars, no padding
+    x = splitmix_bytes(108, 0, 3 * DEC_TILE_SMALL)
+    t = oracle.encode(x)          # 4 * DEC_TILE_SMALL chars (small geometry), no padding
     positions = list(range(4096, 4096 + 64)) + [15, 16, 3071, 3072, 16383, 16384, 16385, 32767, t.size - 1, t.size - 2]
     d = to_dev(t)
     cap = b64.b64_decoded_max_len(t.size)

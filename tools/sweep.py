@@ -26,6 +26,7 @@ VARIANTS = {
     "in5": {"B64_STAGES_IN": 5},
     "out3": {"B64_STAGES_OUT": 3},
     "p2": {"B64_SINGLE_PASSES": 2},
+    "p1": {"B64_SINGLE_PASSES": 1},
     "p2_in6": {"B64_SINGLE_PASSES": 2, "B64_STAGES_IN": 6},
     "w4_c4": {"B64_WARPS_C": 4, "B64_CTAS_PER_SM": 4},
     "w16_c1": {"B64_WARPS_C": 16, "B64_CTAS_PER_SM": 1},
