@@ -324,6 +324,10 @@ std::mutex g_mu;
 std::map<int, DevInfo> g_dev;
 
 constexpr int kMaxHostChunks = 256;
+// Host pipeline chunk: 3 x / 4 x this many MiB of encode / decode input
+#ifndef B64_HOST_CHUNK_MB
+#define B64_HOST_CHUNK_MB 8
+#endif
 struct StreamWs {
   DecWs *d_ws = nullptr;
   b64_result *h_res = nullptr;  // mapped pinned
@@ -684,7 +688,7 @@ int64_t b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, uint8_t 
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
   if (w == nullptr || !pipe_setup(w)) return B64_ERR_CUDA;
-  const int64_t C = host_chunk(n, int64_t(48) << 20, 48);  // multiple of 3 and 16
+  const int64_t C = host_chunk(n, int64_t(3 * B64_HOST_CHUNK_MB) << 20, 48);  // multiple of 3 and 16
   for (int64_t off = 0; off < n; off += C) {
     const int64_t len = n - off < C ? n - off : C;
     const int64_t ooff = off / 3 * 4, olen = 4 * ((len + 2) / 3);
@@ -717,7 +721,7 @@ int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
   if (w == nullptr || !pipe_setup(w)) return B64_ERR_CUDA;
-  const int64_t C = host_chunk(m, int64_t(64) << 20, 64);  // multiple of 4 and 16
+  const int64_t C = host_chunk(m, int64_t(4 * B64_HOST_CHUNK_MB) << 20, 64);  // multiple of 4 and 16
   int nch = 0;
   for (int64_t off = 0; off == 0 || off < m; off += C, ++nch) {
     const int64_t len = m - off < C ? m - off : C;

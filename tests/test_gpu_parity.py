@@ -425,7 +425,7 @@ def test_host_buffer_api():
 
 
 def test_host_buffer_api_multichunk():
-    """Host pipeline over several 48 MiB / 64 MiB chunks: round trip, an
+    """Host pipeline over several 24 MiB / 32 MiB chunks: round trip, an
     error in a middle chunk, '=' at a chunk seam, LENGTH on the last chunk."""
     from tests import oracle_par
 

@@ -73,6 +73,9 @@ VARIANTS = {
     "b_trace": {"B64_BATCH_TRACE": 1},
     "dec_stg32": {"B64_DEC_STG32": 1},
     "dec_slice": {"B64_DEC_STG32": 0},
+    "hc4": {"B64_HOST_CHUNK_MB": 4},
+    "hc2": {"B64_HOST_CHUNK_MB": 2},
+    "hc8": {"B64_HOST_CHUNK_MB": 8},
     "ds_nodefer": {"B64_DS_DEFER": 0},
     "ws_nodirect": {"B64_WS_DIRECT": 0},
     "b_c2_s2": {"B64_BATCH_CTAS": 2, "B64_BATCH_SLOTS": 2},
