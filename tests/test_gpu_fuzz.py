@@ -250,3 +250,32 @@ def test_fuzz_host_buffers():
         rst, rep, rout = oracle.decode(c)
         assert (st, ep, ol) == (rst, rep, rout.size), ("host decode", case, st, ep, rst, rep)
         assert np.array_equal(hy.numpy()[:ol], rout), ("host decode bytes", case)
+
+
+@pytest.mark.parametrize("k,hi", [(2_000_000, 100), (300_000, 2000)])
+def test_batched_many_messages(k, hi):
+    """Millions of tiny messages (per-warp first-message table, walker
+    windows, plan chunks of thousands of messages per CTA): every sampled
+    message and every corrupted one matches the oracle."""
+    rng = np.random.default_rng(9006 + k)
+    lens = rng.integers(0, hi, k).astype(np.int64)
+    off = np.zeros(k + 1, dtype=np.int64)
+    off[1:] = np.cumsum(lens)
+    raw = splitmix_bytes(9006, 0, int(off[-1]))
+    out, oo = b64.b64_encode_batch(to_dev(raw), torch.from_numpy(off).to(DEV))
+    o, oo = host(out), host(oo)
+    idx = rng.choice(k, 1500, replace=False)
+    for i in idx:
+        assert np.array_equal(o[oo[i]:oo[i + 1]], oracle.encode(raw[off[i]:off[i + 1]])), (k, i)
+    cat = o[:oo[k]].copy()
+    toff = oo.astype(np.int64)
+    bad = rng.choice(k, 1000, replace=False)
+    for i in bad:
+        if toff[i + 1] > toff[i]:
+            cat[int(rng.integers(toff[i], toff[i + 1]))] = ord("!")
+    y, yo, yl, ye, ys = b64.b64_decode_batch(to_dev(cat), torch.from_numpy(toff).to(DEV))
+    y, yo, yl, ye, ys = host(y), host(yo), host(yl), host(ye), host(ys)
+    for i in np.concatenate([idx, bad]):
+        rst, rep, rout = oracle.decode(cat[toff[i]:toff[i + 1]])
+        assert (ys[i], ye[i], yl[i]) == (rst, rep, rout.size), (k, i)
+        assert np.array_equal(y[yo[i]:yo[i] + yl[i]], rout), (k, i)
