@@ -2,7 +2,8 @@
 // (BASELINE.json configs[1]).
 //
 // Work is split into *units*: one unit = kBatchPasses passes of one warp
-// (encode: 1536 input bytes -> 2048 chars; decode: 2048 chars -> 1536 bytes).
+// (kBatchPasses = 6: encode 2304 input bytes -> 3072 chars; decode 3072
+// chars -> 2304 bytes).
 // A unit never straddles messages, so a message of len bytes has
 // ceil(len / unit) units (at most one partial unit per message, <= 2-4 %
 // slack at data-URI sizes).  The planner scans the message lengths once

@@ -23,7 +23,7 @@ namespace b64 {
 #define B64_SINGLE_PASSES 4
 #endif
 #ifndef B64_BATCH_PASSES  // passes of one warp per batched work unit
-#define B64_BATCH_PASSES 4
+#define B64_BATCH_PASSES 6
 #endif
 #ifndef B64_BATCH_SLOTS   // per-warp input ring depth (batched)
 #define B64_BATCH_SLOTS 2

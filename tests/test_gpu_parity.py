@@ -339,7 +339,9 @@ def check_decode_batch(text, off, in_mis=0):
 
 def test_batch_encode_decode_ragged():
     rng = np.random.default_rng(114)
-    lens = np.concatenate([np.arange(0, 70), rng.integers(0, 30000, 200), [6144, 6145, 12288, 65536]])
+    # batched units: 2304 input bytes / 3072 chars (6 passes of one warp)
+    lens = np.concatenate([np.arange(0, 70), rng.integers(0, 30000, 200),
+                           [2303, 2304, 2305, 4608, 4609, 6144, 6145, 6912, 12288, 65536]])
     rng.shuffle(lens)
     for start, mis in ((0, 0), (5, 3), (1, 0)):
         raw, off = _batch_case(lens, 114, start=start)

@@ -74,6 +74,12 @@ VARIANTS = {
     "dec_stg32": {"B64_DEC_STG32": 1},
     "dec_slice": {"B64_DEC_STG32": 0},
     "hc4": {"B64_HOST_CHUNK_MB": 4},
+    "b_p6s2": {"B64_BATCH_PASSES": 6},
+    "b_p8s2": {"B64_BATCH_PASSES": 8},
+    "b_p7s2": {"B64_BATCH_PASSES": 7},
+    "b_p5s2": {"B64_BATCH_PASSES": 5},
+    "b_p3s2": {"B64_BATCH_PASSES": 3},
+    "b_p6s3": {"B64_BATCH_PASSES": 6, "B64_BATCH_SLOTS": 3},
     "hc2": {"B64_HOST_CHUNK_MB": 2},
     "hc8": {"B64_HOST_CHUNK_MB": 8},
     "ds_nodefer": {"B64_DS_DEFER": 0},
