@@ -317,8 +317,10 @@ using namespace b64;
 
 struct DevInfo {
   int sms = 0;
+  int wl_ctas = 1;  // resident decode_lines_kernel CTAs per SM
   bool attrs_set = false;
 };
+int g_wl_ctas = 1;
 
 std::mutex g_mu;
 std::map<int, DevInfo> g_dev;
@@ -405,6 +407,11 @@ bool device_setup(int *dev_out, int *sms_out) {
     if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return false;
     if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return false;
     if (set_smem(decode_lines_kernel, sizeof(WlSmem)) != cudaSuccess) return false;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.wl_ctas, decode_lines_kernel, kWlThreads,
+                                                      sizeof(WlSmem)) != cudaSuccess ||
+        di.wl_ctas < 1)
+      di.wl_ctas = 1;
+    g_wl_ctas = di.wl_ctas;
     if (set_smem(encode_wrap_kernel<2, true>, sizeof(WrSmem)) != cudaSuccess) return false;
     if (set_smem(encode_wrap_kernel<2, false>, sizeof(WrSmem)) != cudaSuccess) return false;
     if (set_smem(encode_wrap_kernel<1, false>, sizeof(WrSmem)) != cudaSuccess) return false;
@@ -849,7 +856,7 @@ int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
   // general path, which returns at once when 1. succeeded.
   WlState *wl = reinterpret_cast<WlState *>(base + kWlStateOffset);
   if (cudaMemsetAsync(wl, 0, sizeof(WlState), stream) != cudaSuccess) return B64_ERR_CUDA;
-  decode_lines_kernel<<<static_cast<unsigned>(sms) * 2, kWlThreads, sizeof(WlSmem), stream>>>(
+  decode_lines_kernel<<<static_cast<unsigned>(sms * g_wl_ctas), kWlThreads, sizeof(WlSmem), stream>>>(
       d_in, m, d_out, wl, d_result, flags);
   cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(
       d_in, m, tpc, counts, masks, &hdr->errkey, &wl->verdict);

@@ -29,7 +29,7 @@ namespace b64 {
 constexpr int kWlWarps = 16;                       // compute warps
 constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #ifndef B64_WL_TILE
-#define B64_WL_TILE 28672
+#define B64_WL_TILE 77824
 #endif
 #ifndef B64_WL_SLEEP  // producer back-off between empty-slot polls (ns); 0 = try_wait loop
 #define B64_WL_SLEEP 0
@@ -134,7 +134,14 @@ __global__ void __launch_bounds__(kWlThreads, 2)
   bool viol = !ok;
   if (ok) {
     const int Sl = L + e, G = L / 4;
-    const int Lt = kWlTile / Sl;                          // lines per tile
+    // lines per tile: as many as fit (large tiles amortise the per-tile
+    // work -- 28 KiB: 0.616 ms, 76 KiB: 0.529 ms on the mime workload), but
+    // at least two tiles per CTA for small inputs
+    int Lt = kWlTile / Sl;
+    {
+      const int64_t want = (nlines + 2 * static_cast<int64_t>(gridDim.x) - 1) / (2 * static_cast<int64_t>(gridDim.x));
+      if (want < Lt) Lt = want < 1 ? 1 : static_cast<int>(want);
+    }
     const int64_t ntiles = (nlines + Lt - 1) / Lt;
     const int64_t Q = Mc / 4;                             // complete quads
     const bool pads_ok = (Mc & 3) == 0;

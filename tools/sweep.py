@@ -74,6 +74,22 @@ VARIANTS = {
     "dec_stg32": {"B64_DEC_STG32": 1},
     "dec_slice": {"B64_DEC_STG32": 0},
     "hc4": {"B64_HOST_CHUNK_MB": 4},
+    "wl_t20": {"B64_WL_TILE": 20480},
+    "wl_t36": {"B64_WL_TILE": 36864},
+    "wl_t40": {"B64_WL_TILE": 40960},
+    "wl_t44": {"B64_WL_TILE": 45056},
+    "wl_t52": {"B64_WL_TILE": 53248},
+    "wl_t60": {"B64_WL_TILE": 61440},
+    "wl_t68": {"B64_WL_TILE": 69632},
+    "wl_t72": {"B64_WL_TILE": 73728},
+    "wl_t76": {"B64_WL_TILE": 77824},
+    "wl_t48": {"B64_WL_TILE": 49152},
+    "wl_t56": {"B64_WL_TILE": 57344},
+    "wl_t32": {"B64_WL_TILE": 32768},
+    "wl_s3": {"B64_WL_STAGES": 3, "B64_WL_TILE": 20480},
+    "wr_st3": {"B64_WR_STAGES": 3, "B64_WR_IN": 16384, "B64_WR_OUT": 22528},
+    "wr_big": {"B64_WR_IN": 27648, "B64_WR_OUT": 36864},
+    "cp_w8": {"B64_CP_WARPS": 8, "B64_CP_CTAS": 4},
     "b_p6s2": {"B64_BATCH_PASSES": 6},
     "b_p8s2": {"B64_BATCH_PASSES": 8},
     "b_p7s2": {"B64_BATCH_PASSES": 7},
