@@ -41,7 +41,10 @@ constexpr int kCpWords = kCpTile / 4;               // 4096 words
 constexpr int kCpWarpWords = kCpWords / kCpWarps;   // 256 words = 1 KiB per warp
 constexpr int kCpPerLane = kCpWarpWords / 32;       // 8 words per lane
 static_assert(kCpPerLane == 8, "compact_tile packs 8 keep nibbles per lane");
-constexpr int kCpStages = 3;                        // TMA input ring depth
+#ifndef B64_CP_STAGES
+#define B64_CP_STAGES 3
+#endif
+constexpr int kCpStages = B64_CP_STAGES;            // TMA input ring depth
 #ifndef B64_CP_CTAS
 #define B64_CP_CTAS 2
 #endif

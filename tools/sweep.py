@@ -24,6 +24,10 @@ VARIANTS = {
     "store_ef": {"B64_STORE_EVICT_FIRST": 1},
     "in3": {"B64_STAGES_IN": 3},
     "in5": {"B64_STAGES_IN": 5},
+    "in4": {"B64_STAGES_IN": 4},
+    "cps4": {"B64_CP_STAGES": 4},
+    "cps2": {"B64_CP_STAGES": 2},
+    "in2": {"B64_STAGES_IN": 2},
     "out3": {"B64_STAGES_OUT": 3},
     "p2": {"B64_SINGLE_PASSES": 2},
     "p1": {"B64_SINGLE_PASSES": 1},
@@ -89,6 +93,8 @@ VARIANTS = {
     "wl_s3": {"B64_WL_STAGES": 3, "B64_WL_TILE": 20480},
     "wr_st3": {"B64_WR_STAGES": 3, "B64_WR_IN": 16384, "B64_WR_OUT": 22528},
     "wr_big": {"B64_WR_IN": 27648, "B64_WR_OUT": 36864},
+    "wr_huge": {"B64_WR_IN": 43008, "B64_WR_OUT": 57344},
+    "wr_s3": {"B64_WR_STAGES": 3, "B64_WR_IN": 30720, "B64_WR_OUT": 40960},
     "cp_w8": {"B64_CP_WARPS": 8, "B64_CP_CTAS": 4},
     "b_p6s2": {"B64_BATCH_PASSES": 6},
     "b_p8s2": {"B64_BATCH_PASSES": 8},
