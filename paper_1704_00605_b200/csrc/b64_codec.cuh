@@ -35,7 +35,7 @@ namespace b64 {
 #define B64_BATCH_CTAS 1
 #endif
 #ifndef B64_BATCH_WARPS   // warps per CTA (batched)
-#define B64_BATCH_WARPS 16
+#define B64_BATCH_WARPS 20
 #endif
 #ifndef B64_CTAS_PER_SM
 #define B64_CTAS_PER_SM 1

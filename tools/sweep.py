@@ -26,6 +26,18 @@ VARIANTS = {
     "in5": {"B64_STAGES_IN": 5},
     "in4": {"B64_STAGES_IN": 4},
     "cps4": {"B64_CP_STAGES": 4},
+    "bw12": {"B64_BATCH_WARPS": 12},
+    "bw20": {"B64_BATCH_WARPS": 20},
+    "bw24": {"B64_BATCH_WARPS": 24, "B64_BATCH_PASSES": 4},
+    "bw20p5": {"B64_BATCH_WARPS": 20, "B64_BATCH_PASSES": 5},
+    "bw20s3": {"B64_BATCH_WARPS": 20, "B64_BATCH_SLOTS": 3},
+    "bw18": {"B64_BATCH_WARPS": 18},
+    "bw22": {"B64_BATCH_WARPS": 22},
+    "wl_nb10": {"B64_WL_BATCH": 10},
+    "wl_nb8": {"B64_WL_BATCH": 8},
+    "wl_nb7": {"B64_WL_BATCH": 7},
+    "wl_nb5": {"B64_WL_BATCH": 5},
+    "wl_nb4": {"B64_WL_BATCH": 4},
     "cps2": {"B64_CP_STAGES": 2},
     "in2": {"B64_STAGES_IN": 2},
     "out3": {"B64_STAGES_OUT": 3},
