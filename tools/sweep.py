@@ -30,6 +30,9 @@ VARIANTS = {
     "bw20": {"B64_BATCH_WARPS": 20},
     "bw24": {"B64_BATCH_WARPS": 24, "B64_BATCH_PASSES": 4},
     "bw20p5": {"B64_BATCH_WARPS": 20, "B64_BATCH_PASSES": 5},
+    "b_p7": {"B64_BATCH_PASSES": 7},
+    "sw20": {"B64_WARPS_C": 20},
+    "sw12": {"B64_WARPS_C": 12},
     "bw20s3": {"B64_BATCH_WARPS": 20, "B64_BATCH_SLOTS": 3},
     "bw18": {"B64_BATCH_WARPS": 18},
     "bw22": {"B64_BATCH_WARPS": 22},
