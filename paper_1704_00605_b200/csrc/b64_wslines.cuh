@@ -26,7 +26,10 @@
 
 namespace b64 {
 
-constexpr int kWlWarps = 16;                       // compute warps
+#ifndef B64_WL_WARPS
+#define B64_WL_WARPS 16
+#endif
+constexpr int kWlWarps = B64_WL_WARPS;             // compute warps
 constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #ifndef B64_WL_TILE
 #define B64_WL_TILE 77824
@@ -67,7 +70,7 @@ struct alignas(128) WlSmem {
   int32_t flag;
 };
 
-__global__ void __launch_bounds__(kWlThreads, 2)
+__global__ void __launch_bounds__(kWlThreads, 1)
     decode_lines_kernel(const uint8_t *__restrict__ in, int64_t M, uint8_t *__restrict__ out,
                         WlState *st, b64_result *res, int flags) {
   extern __shared__ __align__(128) uint8_t smem_raw[];

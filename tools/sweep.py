@@ -32,6 +32,9 @@ VARIANTS = {
     "bw20p5": {"B64_BATCH_WARPS": 20, "B64_BATCH_PASSES": 5},
     "b_p7": {"B64_BATCH_PASSES": 7},
     "sw20": {"B64_WARPS_C": 20},
+    "wlw24": {"B64_WL_WARPS": 24},
+    "wlw30": {"B64_WL_WARPS": 30},
+    "wlw12": {"B64_WL_WARPS": 12},
     "sw12": {"B64_WARPS_C": 12},
     "bw20s3": {"B64_BATCH_WARPS": 20, "B64_BATCH_SLOTS": 3},
     "bw18": {"B64_BATCH_WARPS": 18},
