@@ -46,6 +46,9 @@ namespace b64 {
 #ifndef B64_ENC_ARITH  // measurement only: Table I mapping by SWAR arithmetic instead of the table
 #define B64_ENC_ARITH 0
 #endif
+#ifndef B64_DEC_STG64  // with B64_DEC_STG32: one 8-byte + one 4-byte store per 12-byte run
+#define B64_DEC_STG64 0
+#endif
 #ifndef B64_DEC_STG32  // decode DIRECT tiles: three 4-byte stores from registers (no smem slice)
 #define B64_DEC_STG32 1
 #endif
@@ -415,10 +418,20 @@ __device__ __forceinline__ uint32_t decode_tile(const uint8_t *sin, int L, uint8
 #if B64_DEC_STG32
     if constexpr (DIRECT) {  // three 4-byte stores straight from registers (lanes 12 B apart)
       if (FULL || (active && bo + 12 <= olim)) {
+#if B64_DEC_STG64
+        // 12 bytes as one 8-byte + one 4-byte store: even threads' runs are
+        // 8-byte aligned ([8][4]), odd threads' are not ([4][8])
+        const bool ev = ((reinterpret_cast<uintptr_t>(gdst + bo)) & 7) == 0;
+        uint8_t *g8 = gdst + bo + (ev ? 0 : 4);
+        uint8_t *g4 = gdst + bo + (ev ? 8 : 0);
+        *reinterpret_cast<uint2 *>(g8) = ev ? make_uint2(o[0], o[1]) : make_uint2(o[1], o[2]);
+        *reinterpret_cast<uint32_t *>(g4) = ev ? o[2] : o[0];
+#else
         uint32_t *g = reinterpret_cast<uint32_t *>(gdst + bo);
         g[0] = o[0];
         g[1] = o[1];
         g[2] = o[2];
+#endif
       } else if (active) {  // the run holding the stream's padded final quad: its olim - bo bytes
         for (int j = 0; j < olim - bo; ++j) {
           const uint32_t w = j < 4 ? o[0] : j < 8 ? o[1] : o[2];

@@ -95,6 +95,7 @@ VARIANTS = {
     "b_trace": {"B64_BATCH_TRACE": 1},
     "dec_stg32": {"B64_DEC_STG32": 1},
     "dec_slice": {"B64_DEC_STG32": 0},
+    "dec_stg64": {"B64_DEC_STG64": 1},
     "hc4": {"B64_HOST_CHUNK_MB": 4},
     "wl_t20": {"B64_WL_TILE": 20480},
     "wl_t36": {"B64_WL_TILE": 36864},
