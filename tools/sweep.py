@@ -26,6 +26,8 @@ VARIANTS = {
     "in5": {"B64_STAGES_IN": 5},
     "in4": {"B64_STAGES_IN": 4},
     "cps4": {"B64_CP_STAGES": 4},
+    "wl_nb12": {"B64_WL_BATCH": 12},
+    "wr_b3": {"B64_WR_BATCH": 3},
     "bw12": {"B64_BATCH_WARPS": 12},
     "bw20": {"B64_BATCH_WARPS": 20},
     "bw24": {"B64_BATCH_WARPS": 24, "B64_BATCH_PASSES": 4},
