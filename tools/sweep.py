@@ -26,6 +26,9 @@ VARIANTS = {
     "in5": {"B64_STAGES_IN": 5},
     "in4": {"B64_STAGES_IN": 4},
     "cps4": {"B64_CP_STAGES": 4},
+    "cp_w32": {"B64_CP_WARPS": 32, "B64_CP_CTAS": 1},
+    "cp_w24": {"B64_CP_WARPS": 24, "B64_CP_CTAS": 1},
+    "cp_w12": {"B64_CP_WARPS": 12, "B64_CP_CTAS": 2},
     "wl_nb12": {"B64_WL_BATCH": 12},
     "wr_b3": {"B64_WR_BATCH": 3},
     "bw12": {"B64_BATCH_WARPS": 12},
