@@ -40,6 +40,10 @@ constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #ifndef B64_WL_BATCH  // interior loop: quads per thread whose loads are issued together (0 = off)
 #define B64_WL_BATCH 6
 #endif
+#ifndef B64_WL_DIRECT  // interior tiles: shuffle-packed 4-byte stores from registers
+#define B64_WL_DIRECT 1
+#endif
+constexpr bool kWlDirect = B64_WL_DIRECT != 0;
 #ifndef B64_WL_STAGES
 #define B64_WL_STAGES 2
 #endif
@@ -144,6 +148,9 @@ __global__ void __launch_bounds__(kWlThreads, 1)
     {
       const int64_t want = (nlines + 2 * static_cast<int64_t>(gridDim.x) - 1) / (2 * static_cast<int64_t>(gridDim.x));
       if (want < Lt) Lt = want < 1 ? 1 : static_cast<int>(want);
+      // a multiple of 4 lines: 3 * (first quad of a tile) is then a multiple
+      // of 4, so DIRECT stores stay 4-byte aligned in every tile
+      if (kWlDirect) Lt = Lt < 4 ? 4 : Lt & ~3;
     }
     const int64_t ntiles = (nlines + Lt - 1) / Lt;
     const int64_t Q = Mc / 4;                             // complete quads
@@ -183,6 +190,10 @@ __global__ void __launch_bounds__(kWlThreads, 1)
       const int dl32 = 32 / G, dc32 = 32 % G;
       const int pstep = dl32 * Sl + 4 * dc32;
       uint8_t *slice = S.out[warp];
+      // DIRECT packing: word j (lane j < 24) of a 96-byte run holds output
+      // bytes 4j..4j+3 = bytes r.. of lane ps's 3 and the rest of lane ps+1's
+      const int ps = lane < 24 ? (4 * lane) / 3 : 0, pr = 4 * lane - 3 * ps;
+      const uint32_t psel = pr == 0 ? 0x4210u : (pr == 1 ? 0x5421u : 0x6542u);
       int k = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
         const int s = k % kWlStages;
@@ -210,7 +221,83 @@ __global__ void __launch_bounds__(kWlThreads, 1)
           uint8_t *ob = slice + omis - 3 * qa;  // quad q -> ob + 3q
           uint32_t bad = 0;
           const bool interior = q1 < Q && (line0 + Lt) * static_cast<int64_t>(Sl) <= M;
-          if (interior && qa < qb) {
+          // DIRECT (B64_WL_DIRECT, 4-byte aligned output): interior warps pack
+          // 32 lanes' 3-byte results into 24 words with two shuffles and write
+          // them with one coalesced 4-byte store per lane -- no staging slice,
+          // no copy-out (3 STS.U8 + 0.75 LDS.128 per 32 quads -> 2 SHFL)
+          const bool direct = kWlDirect && interior && ((reinterpret_cast<uintptr_t>(gdst) & 3) == 0);
+          if (direct && qa < qb) {
+            int q = qa + lane;
+            int ln = line_of(q), col = q - ln * G;
+            int a = imis + ln * Sl + 4 * col;
+            uint32_t *gw = reinterpret_cast<uint32_t *>(gdst) + lane;  // word lane of each 96-byte run
+            int qs = qa;  // first quad of the warp's current 32-quad row
+            constexpr int NB = B64_WL_BATCH > 0 ? B64_WL_BATCH : 1;
+            for (; qs + 32 * NB <= qb; qs += 32 * NB) {
+              uint32_t wv[NB];
+#pragma unroll
+              for (int j = 0; j < NB; ++j) {
+                wv[j] = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+                a += pstep;
+                col += dc32;
+                if (col >= G) {
+                  col -= G;
+                  a += e;
+                }
+              }
+              uint32_t vv[NB][4];
+#pragma unroll
+              for (int j = 0; j < NB; ++j) {
+                vv[j][0] = lds_u8((wv[j] & 0xFFu) | tb);
+                vv[j][1] = lds_u8(__byte_perm(wv[j], tb, 0x7651));
+                vv[j][2] = lds_u8(__byte_perm(wv[j], tb, 0x7652));
+                vv[j][3] = lds_u8(__byte_perm(wv[j], tb, 0x7653));
+              }
+#pragma unroll
+              for (int j = 0; j < NB; ++j) {
+                bad |= vv[j][0] | vv[j][1] | vv[j][2] | vv[j][3];
+                const uint32_t V = ((vv[j][0] * 64u + vv[j][1]) * 64u + vv[j][2]) * 64u + vv[j][3];
+                const uint32_t b = __byte_perm(V, 0u, 0x4012);  // output bytes 3l..3l+2, little-endian
+                const uint32_t x = __shfl_sync(0xffffffffu, b, ps);
+                const uint32_t y = __shfl_sync(0xffffffffu, b, ps + 1);
+                if (lane < 24) gw[24 * j] = __byte_perm(x, y, psel);
+              }
+              gw += 24 * NB;
+              q += 32 * NB;
+            }
+            for (; qs < qb; qs += 32) {
+              const bool act = q < qb;
+              uint32_t V = 0;
+              if (act) {
+                const uint32_t w = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+                const uint32_t v0 = lds_u8((w & 0xFFu) | tb);
+                const uint32_t v1 = lds_u8(__byte_perm(w, tb, 0x7651));
+                const uint32_t v2 = lds_u8(__byte_perm(w, tb, 0x7652));
+                const uint32_t v3 = lds_u8(__byte_perm(w, tb, 0x7653));
+                bad |= v0 | v1 | v2 | v3;
+                V = ((v0 * 64u + v1) * 64u + v2) * 64u + v3;
+              }
+              if (qs + 32 <= qb) {
+                const uint32_t b = __byte_perm(V, 0u, 0x4012);
+                const uint32_t x = __shfl_sync(0xffffffffu, b, ps);
+                const uint32_t y = __shfl_sync(0xffffffffu, b, ps + 1);
+                if (lane < 24) *gw = __byte_perm(x, y, psel);
+              } else if (act) {  // the warp's ragged last row: byte stores
+                uint8_t *p = gdst + 3 * (q - qa);
+                p[0] = static_cast<uint8_t>(V >> 16);
+                p[1] = static_cast<uint8_t>(V >> 8);
+                p[2] = static_cast<uint8_t>(V);
+              }
+              gw += 24;
+              q += 32;
+              a += pstep;
+              col += dc32;
+              if (col >= G) {
+                col -= G;
+                a += e;
+              }
+            }
+          } else if (interior && qa < qb) {
             // all lines full with an EOL, no final quad: incremental walk
             int q = qa + lane;
             int ln = line_of(q), col = q - ln * G;
@@ -309,7 +396,7 @@ __global__ void __launch_bounds__(kWlThreads, 1)
               S.flag = 1;
               atomicExch(&st->viol, 1);
             }
-          } else if (qa < qb) {
+          } else if (qa < qb && !direct) {
             // this warp's bytes: congruent staging -> 16-byte stores + byte edges
             __syncwarp();
             const int n = 3 * (qb - qa);

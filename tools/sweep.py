@@ -164,6 +164,8 @@ VARIANTS = {
     "b_trace_find": {"B64_BATCH_TRACE": 1, "B64_BATCH_FINDMSG": 1},
     "b_trace_skel": {"B64_BATCH_TRACE": 1, "B64_SKELETON": 1},
     "b_w20_skel": {"B64_BATCH_WARPS": 20, "B64_SKELETON": 1},
+    "wl_nodirect": {"B64_WL_DIRECT": 0},
+    "wl_direct": {"B64_WL_DIRECT": 1},
     "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
 }
 
