@@ -164,6 +164,10 @@ VARIANTS = {
     "b_trace_find": {"B64_BATCH_TRACE": 1, "B64_BATCH_FINDMSG": 1},
     "b_trace_skel": {"B64_BATCH_TRACE": 1, "B64_SKELETON": 1},
     "b_w20_skel": {"B64_BATCH_WARPS": 20, "B64_SKELETON": 1},
+    "wr_base": {"B64_WR_BATCH": 2},
+    "wr_s3_16": {"B64_WR_STAGES": 3, "B64_WR_IN": 16384, "B64_WR_OUT": 22528},
+    "wr_b4n": {"B64_WR_BATCH": 4},
+    "wr_b1n": {"B64_WR_BATCH": 1},
     "wl_nodirect": {"B64_WL_DIRECT": 0},
     "wl_direct": {"B64_WL_DIRECT": 1},
     "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
