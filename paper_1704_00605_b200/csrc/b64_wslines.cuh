@@ -38,7 +38,7 @@ constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #define B64_WL_SLEEP 0
 #endif
 #ifndef B64_WL_BATCH  // interior loop: quads per thread whose loads are issued together (0 = off)
-#define B64_WL_BATCH 6
+#define B64_WL_BATCH 4
 #endif
 #ifndef B64_WL_DIRECT  // interior tiles: shuffle-packed 4-byte stores from registers
 #define B64_WL_DIRECT 1

@@ -168,6 +168,8 @@ VARIANTS = {
     "wr_s3_16": {"B64_WR_STAGES": 3, "B64_WR_IN": 16384, "B64_WR_OUT": 22528},
     "wr_b4n": {"B64_WR_BATCH": 4},
     "wr_b1n": {"B64_WR_BATCH": 1},
+    "wl_b2": {"B64_WL_BATCH": 2},
+    "wl_b3": {"B64_WL_BATCH": 3},
     "wl_nodirect": {"B64_WL_DIRECT": 0},
     "wl_direct": {"B64_WL_DIRECT": 1},
     "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
