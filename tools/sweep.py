@@ -170,6 +170,8 @@ VARIANTS = {
     "wr_b1n": {"B64_WR_BATCH": 1},
     "wl_b2": {"B64_WL_BATCH": 2},
     "wl_b3": {"B64_WL_BATCH": 3},
+    "wr_bulk0": {"B64_WR_BULK": 0},
+    "wr_bulk1": {"B64_WR_BULK": 1},
     "wl_nodirect": {"B64_WL_DIRECT": 0},
     "wl_direct": {"B64_WL_DIRECT": 1},
     "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
