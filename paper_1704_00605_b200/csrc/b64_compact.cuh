@@ -240,7 +240,9 @@ __device__ __forceinline__ void cp_load(CpSmem &S, const CpGeom &G, const uint32
 // (the compiler keeps shared loads below earlier shared stores otherwise,
 // which puts a load latency on every word) -- measured faster in the fused
 // decode (1.068 -> 1.057 ms), marginally slower in despace (0.811 vs 0.816).
-template <bool PIPE>
+// WAITB: thread 0 waits for the reads of its earlier bulk stores (the copy-out
+// of the stream this call overwrites) just before the internal barrier.
+template <bool PIPE, bool WAITB = false>
 __device__ __forceinline__ int compact_tile(const uint8_t *win, const uint32_t *msk,
                                             uint8_t *stream, int dst, int32_t *wcnt,
                                             const uint32_t *ktab) {
@@ -269,6 +271,7 @@ __device__ __forceinline__ int compact_tile(const uint8_t *win, const uint32_t *
                      ((T1 >> 8) & 0x00FF00FFu);
   const int wtot = static_cast<int>((h & 0xFFFFu) + (h >> 16));
   if (lane == 0) wcnt[warp] = wtot;
+  if (WAITB && tid == 0) ptx::bulk_wait_read<0>();
   __syncthreads();
   const int c = lane < kCpWarps ? wcnt[lane] : 0;
   int incl = c;
@@ -337,9 +340,38 @@ __device__ __forceinline__ void cta_copy_out_congruent(uint8_t *dst, const uint8
   }
 }
 
+// The same copy with the 16-byte aligned interior as one bulk (TMA) store
+// issued by thread 0 (committed as one bulk group; the caller waits with
+// bulk_wait_read before the staging is overwritten and with bulk_wait before
+// the CTA exits) and the edges as byte stores by threads 32.. and 64.. .
+// The staging writes must be fenced to the async proxy
+// (fence_proxy_async_smem) by their writers before the barrier preceding
+// this call.  Frees the CTA's threads from the copy-out loop.
+__device__ __forceinline__ void cta_copy_out_bulk(uint8_t *dst, const uint8_t *src, int n,
+                                                  uint64_t pol) {
+  const int tid = threadIdx.x;
+  const uintptr_t g = reinterpret_cast<uintptr_t>(dst);
+  const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
+  const uintptr_t a1 = (g + static_cast<uintptr_t>(n)) & ~static_cast<uintptr_t>(15);
+  if (a1 > a0) {
+    const int head = static_cast<int>(a0 - g), tail0 = static_cast<int>(a1 - g);
+    if (tid == 0) {
+      ptx::bulk_s2g(reinterpret_cast<void *>(a0), src + head, static_cast<uint32_t>(a1 - a0), pol);
+      ptx::bulk_commit();
+    }
+    if (tid >= 32 && tid - 32 < head) dst[tid - 32] = src[tid - 32];
+    if (tid >= 64 && tid - 64 < n - tail0) dst[tail0 + tid - 64] = src[tail0 + tid - 64];
+  } else if (tid < n) {
+    dst[tid] = src[tid];
+  }
+}
+
 // ------------------------------------------------------ despace (f3) ---
 #ifndef B64_DS_GROUP
 #define B64_DS_GROUP 1
+#endif
+#ifndef B64_DS_BULK  // copy-out as one bulk store (cta_copy_out_bulk)
+#define B64_DS_BULK 1
 #endif
 #ifndef B64_DS_DEFER  // copy tile t's stream out after tile t+1's compaction barrier
 #define B64_DS_DEFER 1
@@ -381,6 +413,7 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
   int64_t running, total;
   chunk_prefix(counts, gridDim.x, blockIdx.x, running, total, S.red);  // has a __syncthreads
   const uint64_t pol = ptx::policy_evict_first();
+  const uint64_t pol_out = pol;
   // TMA ring of kDsStages tiles (window + masks on one mbarrier each)
   auto load = [&](int64_t t, int s) {
     const int h = G.hi(t);
@@ -405,11 +438,21 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     const int s = it % kDsStages, b = it & 1;
     const int dst = static_cast<int>((obase + static_cast<uintptr_t>(running)) & 15);
     ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((it / kDsStages) & 1));
-    const int n = compact_tile<false>(S.win[s], S.msk[s], S.stream[b], dst, S.wcnt[b], S.ktab);
-    ptx::fence_proxy_async_smem();  // generic reads of win[s] before its next bulk write
+    // (B64_DS_BULK) stream[b]'s bulk store, issued in the previous
+    // iteration, must have read it before compact_tile's barrier releases
+    // the placement stores into it
+    const int n = compact_tile<false, B64_DS_BULK != 0>(S.win[s], S.msk[s], S.stream[b], dst, S.wcnt[b],
+                                                       S.ktab);
+    // generic reads of win[s] before its next bulk write; this tile's stream
+    // writes before the bulk store that reads them (after the next barrier)
+    ptx::fence_proxy_async_smem();
     if (tid == 0 && t + kDsStages - 1 < t1)
       load(t + kDsStages - 1, static_cast<int>((it + kDsStages - 1) % kDsStages));
+#if B64_DS_BULK
+    if (it > 0) cta_copy_out_bulk(out + prun, S.stream[b ^ 1] + pdst, pn, pol_out);
+#else
     if (it > 0) cta_copy_out_congruent(out + prun, S.stream[b ^ 1] + pdst, pn);
+#endif
     prun = running;
     pdst = dst;
     pn = n;
@@ -417,7 +460,12 @@ __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
   }
   if (t1 > t0) {
     __syncthreads();
+#if B64_DS_BULK
+    cta_copy_out_bulk(out + prun, S.stream[(t1 - 1 - t0) & 1] + pdst, pn, pol_out);
+    if (tid == 0) ptx::bulk_wait<0>();
+#else
     cta_copy_out_congruent(out + prun, S.stream[(t1 - 1 - t0) & 1] + pdst, pn);
+#endif
   }
 #else
   int64_t t = t0;

@@ -242,25 +242,9 @@ __global__ void __launch_bounds__(kWrThreads, 2)
 #endif
     __syncthreads();
 #if B64_WR_BULK
-    {
-      // the 16-byte aligned interior leaves with one bulk store (staging is
-      // congruent to the destination mod 16); the edges with byte stores
-      uint8_t *gd = out + dst;
-      const uintptr_t g = reinterpret_cast<uintptr_t>(gd);
-      const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
-      const uintptr_t a1 = (g + static_cast<uintptr_t>(olen)) & ~static_cast<uintptr_t>(15);
-      if (a1 > a0) {
-        const int head = static_cast<int>(a0 - g), tail0 = static_cast<int>(a1 - g);
-        if (tid == 0) {
-          ptx::bulk_s2g(reinterpret_cast<void *>(a0), ob + head, static_cast<uint32_t>(a1 - a0), pol);
-          ptx::bulk_commit();
-        }
-        if (tid >= 32 && tid - 32 < head) gd[tid - 32] = ob[tid - 32];
-        if (tid >= 64 && tid - 64 < olen - tail0) gd[tail0 + tid - 64] = ob[tail0 + tid - 64];
-      } else if (tid < olen) {
-        gd[tid] = ob[tid];
-      }
-    }
+    // the 16-byte aligned interior leaves with one bulk store (staging is
+    // congruent to the destination mod 16), the edges with byte stores
+    cta_copy_out_bulk(out + dst, ob, olen, pol);
 #else
     cta_copy_out_congruent(out + dst, ob, olen);
 #endif

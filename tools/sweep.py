@@ -172,6 +172,8 @@ VARIANTS = {
     "wl_b3": {"B64_WL_BATCH": 3},
     "wr_bulk0": {"B64_WR_BULK": 0},
     "wr_bulk1": {"B64_WR_BULK": 1},
+    "ds_bulk0": {"B64_DS_BULK": 0},
+    "ds_bulk1": {"B64_DS_BULK": 1},
     "wl_nodirect": {"B64_WL_DIRECT": 0},
     "wl_direct": {"B64_WL_DIRECT": 1},
     "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
