@@ -11,7 +11,8 @@
 // take consecutive groups, so the 2-byte / 1-byte stores of a warp hit
 // consecutive shared-memory words), the group's line comes from one
 // multiply-high by a precomputed reciprocal, and the tile's output -- staged
-// congruent to its destination mod 16 -- leaves with 16-byte stores.
+// congruent to its destination mod 16 -- leaves as one bulk (TMA) store
+// of its aligned interior plus byte stores for the edges (B64_WR_BULK).
 #pragma once
 #include <cstdint>
 
