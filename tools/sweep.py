@@ -174,6 +174,9 @@ VARIANTS = {
     "wr_bulk1": {"B64_WR_BULK": 1},
     "ds_bulk0": {"B64_DS_BULK": 0},
     "ds_bulk1": {"B64_DS_BULK": 1},
+    "wl_base": {"B64_WL_TILE": 77824},
+    "wl_s3_40": {"B64_WL_TILE": 40960, "B64_WL_STAGES": 3},
+    "wl_s3_52": {"B64_WL_TILE": 53248, "B64_WL_STAGES": 3},
     "wl_nodirect": {"B64_WL_DIRECT": 0},
     "wl_direct": {"B64_WL_DIRECT": 1},
     "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
