@@ -50,6 +50,37 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def source_hash():
+    """sha256 of the library's sources (csrc/*.cu[h], include/b64gpu.h): the
+    stamp under which profiles/ncu_traffic.json entries were captured."""
+    import hashlib
+
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_1704_00605_b200", "csrc")
+    files = sorted(os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith((".cu", ".cuh")))
+    for f in files + [os.path.join(ROOT, "include", "b64gpu.h")]:
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode())
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def measured_traffic(key):
+    """dram bytes per launch of `key` from profiles/ncu_traffic.json, only
+    if it was captured from the sources being benched (else None, reason)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+    except (OSError, ValueError):
+        return None, "no profiles/ncu_traffic.json"
+    ent = tr.get(key)
+    if not ent:
+        return None, f"no entry {key}"
+    if ent.get("source_sha") != source_hash():
+        return None, f"stale: captured from sources {ent.get('source_sha')}, benched {source_hash()}"
+    return ent.get("dram_bytes_per_launch"), ent.get("source")
+
+
 def cpu_info():
     model = "unknown"
     try:
@@ -170,10 +201,21 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: LOCAL_RANK {local} but only {torch.cuda.device_count()} GPUs visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        # communicator evidence (stderr): one line per rank
+        probe = torch.ones(1, device=dev)
+        dist.all_reduce(probe)
+        print(f"[bench] rank {rank}/{world} on {torch.cuda.get_device_name(dev)} cuda:{local}: NCCL "
+              f"{'.'.join(map(str, torch.cuda.nccl.version()))} process group up, all_reduce(1) = "
+              f"{int(probe.item())}", file=sys.stderr, flush=True)
+        assert int(probe.item()) == world
     b64.load_library()
     stream = torch.cuda.current_stream(dev)
 
@@ -204,8 +246,16 @@ def run_ours(args):
     sptr = ctypes.c_void_p(stream.cuda_stream)
     xp, tp, yp, rp = x.data_ptr(), t.data_ptr(), y.data_ptr(), res.data_ptr()
 
-    err_t = torch.empty(1, dtype=torch.int64, device=dev)
-    lens_parts = [torch.empty(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    # multi-GPU exchange: the shard decode writes its
+    # exchange record (reduction key, out_len) in the kernel finalize; NCCL
+    # reduces the key (MIN) and gathers the lengths; b64_combine_shards_async
+    # writes the whole buffer's result on the device.  No host sync.
+    tbegin = 4 * (begin // 3)                    # global offset of this rank's text shard
+    total_m = b64.b64_encoded_len(total) if wl == "c5" else m
+    key = torch.empty(2, dtype=torch.int64, device=dev)
+    lens = torch.empty(world, dtype=torch.int64, device=dev)
+    gres = b64.result_tensor(dev)
+    kp, lp, gp = key.data_ptr(), lens.data_ptr(), gres.data_ptr()
 
     def step(ev=None):
         if ev is not None:
@@ -215,17 +265,20 @@ def run_ours(args):
             raise RuntimeError(f"encode rc={rc}")
         if ev is not None:
             ev[1].record(stream)
-        rc = lib.b64_decode_shard_async(tp, m, 1 if final else 0, yp, rp, sptr)
+        if world == 1:
+            rc = lib.b64_decode_shard_async(tp, m, 1 if final else 0, yp, rp, sptr)
+        else:
+            rc = lib.b64_decode_shard_ex_async(tp, m, tbegin, 1 if final else 0, yp, 0, rp, kp, sptr)
         if rc < 0:
             raise RuntimeError(f"decode rc={rc}")
         if ev is not None:
             ev[2].record(stream)
         if world > 1:
-            # result exchange: global error offset (MIN) + output lengths (gather)
-            e = res[1:2]
-            torch.where(e >= 0, e + begin, torch.full_like(e, INT64_MAX), out=err_t)
-            dist.all_reduce(err_t, op=dist.ReduceOp.MIN)
-            dist.all_gather(lens_parts, res[0:1])
+            dist.all_reduce(key[0:1], op=dist.ReduceOp.MIN)
+            dist.all_gather_into_tensor(lens, key[1:2])
+            rc = lib.b64_combine_shards_async(kp, lp, world, total_m, gp, sptr)
+            if rc < 0:
+                raise RuntimeError(f"combine rc={rc}")
 
     for _ in range(args.warmup):
         step()
@@ -234,6 +287,9 @@ def run_ours(args):
     ol, ep, st, _ = b64.unpack_result(res)
     if os.environ.get("B64_BENCH_NOCHECK") != "1":   # skeleton variants only (tools/sweep.py)
         assert st == 0 and ep == -1 and ol == n, (st, ep, ol)
+        if world > 1:
+            gol, gep, gst, _ = b64.unpack_result(gres)
+            assert (gst, gep, gol) == (0, -1, total), (gst, gep, gol)
 
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
@@ -272,15 +328,7 @@ def run_ours(args):
     dec_gbs = dec_bytes / (dec_ms / 1e3) / 1e9
     dom = "decode" if dec_ms >= enc_ms else "encode"
     ach = dec_gbs if dom == "decode" else enc_gbs
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        ent = tr.get(f"{wl}:{dom}")
-        if ent:
-            traffic = ent.get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        pass
+    traffic, traffic_src = measured_traffic(f"{wl}:{dom}")
 
     # ---- e2e through the C ABI host-buffer entry points (rank-local sample)
     e2e = None
@@ -312,18 +360,27 @@ def run_ours(args):
                "h2d_bytes_per_step": ns + ms_, "d2h_bytes_per_step": ms_ + ns + 2 * 24,
                "sample": f"{ns} bytes per rank (pinned host) -> b64_encode_host -> b64_decode_host, {reps} steps"}
 
-    # ---- CPU oracle on the host cores (rank 0, N = 1 only)
+    # ---- CPU oracle on the host cores (rank 0; the other ranks wait)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if world > 1:
+        dist.barrier()
+    if rank == 0 and not args.no_cpu:
         smp = min(n, args.cpu_sample)
         smp -= smp % 3
         xs = x[:smp].cpu().numpy()
         gbs, cores, nbytes, el = oracle_threads_bench(xs, reps_min_s=args.cpu_seconds)
+        # the paper's own measurements are single-threaded
+        s1 = min(smp, args.cpu_sample_1core - args.cpu_sample_1core % 3)
+        gbs1, _, nb1, el1 = oracle_threads_bench(xs[:s1], reps_min_s=args.cpu_seconds_1core, threads=1)
         model, ncpu, naff = cpu_info()
         cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle",
                "sample": f"first {smp} bytes of the rank-0 workload: oracle encode + decode of its text, "
                          f"split on 3-byte boundaries over {cores} threads, {el:.1f} s wall",
-               "cpu_model": model, "cpu_count": ncpu}
+               "cpu_model": model, "cpu_count": ncpu,
+               "single_core": {"value": gbs1, "unit": "GB/s", "cores": 1,
+                               "sample": f"first {s1} bytes, one thread, {el1:.1f} s wall (paper: single-threaded, P:1092)"}}
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -336,10 +393,12 @@ def run_ours(args):
                        "parallelism": f"shard x{world}: no data-path collective; MIN all-reduce + length all-gather",
                        "l2": "inputs larger than L2 (126 MB): no flush"},
             "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel", "achieved": ach, "peak": hbm,
-                         "unit": "GB/s", "frac": ach / hbm, "traffic": traffic, "peak_source": hbm_src,
+                         "unit": "GB/s", "frac": ach / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": hbm_src,
                          "algorithmic_bytes_per_launch": dec_bytes if dom == "decode" else enc_bytes},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * K,
-            "gpu_launches_scope": "per rank: 1 encode_kernel + 1 decode_kernel per step",
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (2 if world == 1 else 3) * K,
+            "gpu_launches_scope": "per rank: 1 encode_kernel + 1 decode_kernel per step" + (
+                "" if world == 1 else " + 1 combine_kernel (NCCL all_reduce / all_gather kernels not counted)"),
             "clocks": clocks,
             "detail": {"encode_ms": enc_ms, "decode_ms": dec_ms,
                        "encode_GBps_input": n / (enc_ms / 1e3) / 1e9,
@@ -406,6 +465,7 @@ def run_small_configs(args):
 
     wl = args.workload
     detail = {}
+    kname = {}
     clocks.start()
     if wl == "c1":
         n = W.C1_N
@@ -512,6 +572,7 @@ def run_small_configs(args):
                   "raw_bytes": tot, "text_bytes": mt,
                   "encode_GBps_input": tot / (enc_ms / 1e3) / 1e9, "decode_GBps_input": mt / (dec_ms / 1e3) / 1e9}
         dom, dom_ms = ("encode", enc_ms) if enc_ms >= dec_ms else ("decode", dec_ms)
+        kname = {"encode": "batch_kernel<false>", "decode": "batch_kernel<true>"}
         desc = ("C2: 10,000 messages, log-uniform 100 B - 64 KiB (seed 1): batched encode + batched decode "
                 "(incl. planner); step = one CUDA-graph replay of the two calls")
         launches = 2
@@ -546,6 +607,7 @@ def run_small_configs(args):
         detail = {"despace_ms": ds_ms, "in_bytes": m, "out_bytes": kept,
                   "despace_GBps_input": m / (ds_ms / 1e3) / 1e9}
         dom, dom_ms = "despace", ds_ms
+        kname = {"despace": "b64_despace call (all its kernels)"}
         desc = "f3: whitespace removal of 1.27 GB MIME-style text (76-char lines + CRLF)"
         launches = 2
     elif wl == "mime":
@@ -575,6 +637,7 @@ def run_small_configs(args):
                           "the general mask + compaction kernels return at once); algorithmic bytes = text in + "
                           "bytes out"}
         dom, dom_ms = ("decode_ws", dec_ms) if dec_ms >= enc_ms else ("encode_wrapped", enc_ms)
+        kname = {"decode_ws": "decode_lines_kernel", "encode_wrapped": "encode_wrap_kernel"}
         desc = ("f4: MIME round trip, 57*2^24 random bytes (seed 2) <-> 1.31 GB of 76-char CRLF lines: "
                 "line-wrapped encode + whitespace-tolerant decode")
         launches = 4
@@ -603,6 +666,7 @@ def run_small_configs(args):
                   "decode_ws_GBps_input": m / (dec_ms / 1e3) / 1e9,
                   "note": "general path: fast-path attempt (gives up), mask pass, fused compaction + decode"}
         dom, dom_ms = "decode_ws", dec_ms
+        kname = {"decode_ws": "b64_decode_ws call, general path (all its kernels)"}
         desc = "f4: whitespace-tolerant decode of 1.31 GB of MIME text with irregular line ends (general path)"
         launches = 3
     elif wl == "sweep":
@@ -665,8 +729,8 @@ def run_small_configs(args):
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic: counter-based SplitMix64 bytes (inputs/gen.py), generated on device",
             "config": {"workload": desc, "l2": "flushed before every step: 512 MiB write, then a 256 MiB read (drains the flush's dirty lines)"},
-            "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                         "frac": ach / hbm, "traffic": None, "peak_source": hbm_src},
+            "roofline": {"bound": "hbm", "kernel": kname.get(dom, f"{dom}_kernel"), "achieved": ach, "peak": hbm,
+                         "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": hbm_src},
             "gpu_launches": launches * K, "clocks": clk, "timing": samples, "detail": detail}
     if wl == "sweep":
         line["config"]["l2"] = "not flushed (cache-hot sweep)"
@@ -712,6 +776,24 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a torchrun environment: launch N ranks (one per
+    GPU) of this same command through torch.distributed.run on 127.0.0.1,
+    so that `python bench.py --gpus 8` can never silently measure one GPU.
+    Rank 0's JSON line is the only stdout line; the exit code is the
+    launcher's."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -725,12 +807,23 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=48 << 20)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-sample-1core", type=int, default=12 << 20)
+    ap.add_argument("--cpu-seconds-1core", type=float, default=5.0)
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.warmup < 3 and args.impl == "ours" and os.environ.get("B64_BENCH_ALLOW_FEW_WARMUP") != "1":
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
     elif args.workload in ("c1", "c2", "c4", "despace", "mime", "mime_irregular", "sweep"):
+        if args.gpus != 1:
+            raise SystemExit(f"--workload {args.workload} is a single-GPU parity config; use c5 or c3 for --gpus > 1")
         run_small_configs(args)
     else:
         run_ours(args)

@@ -26,7 +26,15 @@
  *    with the input may be read (never written).  Torch / cudaMalloc
  *    allocations are padded to at least 256 B, so this never leaves the
  *    allocation in practice.
- *  - All entry points are reentrant for calls on distinct streams.
+ *  - Device: every launching call runs on the device that owns `stream`
+ *    (the current device for the legacy / per-thread default stream) and
+ *    restores the caller's current device before returning.
+ *  - All entry points are reentrant for calls on distinct streams.  The
+ *    single-buffer decode keeps its error-reduction scratch per (device,
+ *    stream): two decodes that may run concurrently (e.g. CUDA graphs
+ *    captured on the same stream and replayed at once, or replayed on
+ *    another stream while direct decodes run on the capture stream) must
+ *    have been enqueued on distinct streams.
  */
 #ifndef B64GPU_H
 #define B64GPU_H
@@ -64,7 +72,7 @@ enum {
 typedef struct {
   int64_t out_len;   /* bytes of valid output (see b64_decode)             */
   int64_t err_pos;   /* first error offset, -1 if none                      */
-  int32_t status;    /* b64_status (0, 1 or 2)                              */
+  int32_t status;    /* b64_status >= 0 (OK, INVALID_CHAR, LENGTH, NONCANONICAL) */
   int32_t pad_count; /* number of trailing '=' consumed (0, 1, 2)           */
 } b64_result;
 
@@ -134,9 +142,46 @@ int b64_decode_ex_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
  * (multi-GPU sharder).  final_shard != 0: identical to
  * b64_decode_async.  final_shard == 0: m must be a multiple of 4 and the
  * final-quad padding rule is NOT applied ('=' anywhere is an error), because
- * a later shard follows.  Offsets in d_result are shard-relative. */
+ * a later shard follows (reading R-shard).  Offsets in d_result are
+ * shard-relative. */
 int b64_decode_shard_async(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
                            b64_result *d_result, b64_stream_t stream);
+
+/* b64_decode_shard_async with variant flags (URL applies to every shard;
+ * NOPAD and STRICT change only the final shard's tail) and the exchange
+ * record of the multi-GPU decode: when d_key != NULL the kernel also writes
+ * d_key[0] = b64_shard_key(status, err_pos, shard_begin) (the shard's first
+ * error as a GLOBAL offset with its status, INT64_MAX if clean) and
+ * d_key[1] = out_len (device int64[2], 8-byte aligned).  shard_begin: offset
+ * of d_in[0] in the whole buffer (>= 0).  The MIN all-reduce of d_key[0]
+ * over the shards and the all-gather of d_key[1] are the only exchange;
+ * b64_combine_shards[_async] turns them into the whole buffer's result. */
+int b64_decode_shard_ex_async(const uint8_t *d_in, int64_t m, int64_t shard_begin, int final_shard,
+                              uint8_t *d_out, int flags, b64_result *d_result, int64_t *d_key,
+                              b64_stream_t stream);
+
+/* Reduction key of one shard result: (shard_begin + err_pos) * 4 + status
+ * for status != B64_OK, INT64_MAX for B64_OK.  Shards cover disjoint
+ * offsets, so the minimum key over all shards is the buffer's first error
+ * together with its status.  Pure host. */
+int64_t b64_shard_key(int32_t status, int64_t err_pos, int64_t shard_begin);
+
+/* The whole buffer's decode result from key_min (the MIN over shards of
+ * b64_shard_key) and the shard output lengths h_shard_out_len[0..world):
+ * clean -> status OK, err_pos -1, out_len = sum of the lengths, pad_count =
+ * 3*(total_m/4) - out_len when total_m % 4 == 0 (else 0); error -> err_pos =
+ * key_min / 4, status = key_min % 4, out_len = 3*floor(err_pos/4) (Alg 2
+ * appends nothing for the failing quad).  total_m: characters of
+ * the whole buffer.  Pure host; B64_ERR_ARG on bad arguments. */
+int b64_combine_shards(int64_t key_min, const int64_t *h_shard_out_len, int world, int64_t total_m,
+                       b64_result *h_result);
+
+/* The same on the device (one tiny kernel on `stream`): d_key_min (int64),
+ * d_shard_out_len (int64[world]) and d_result are device pointers, so the
+ * whole sharded step -- decode, NCCL MIN all-reduce, all-gather, combine --
+ * runs without a host synchronization. */
+int b64_combine_shards_async(const int64_t *d_key_min, const int64_t *d_shard_out_len, int world,
+                             int64_t total_m, b64_result *d_result, b64_stream_t stream);
 
 /* ---------------------------------------------------------------- batched */
 
@@ -149,9 +194,10 @@ size_t b64_batch_workspace_bytes(int64_t k, int64_t total_in, int direction);
  * d_in[d_in_off[i] .. d_in_off[i+1]) (d_in_off: k+1 non-decreasing int64 on
  * the device, d_in_off[0] may be > 0).  Writes d_out_off[0..k] (device,
  * d_out_off[0] = 0, d_out_off[i+1]-d_out_off[i] = b64_encoded_len(len_i))
- * and each encoding contiguously to d_out.  Messages are split into tiles
- * assigned to CTAs by the prefix sums of their lengths (BASELINE.json
- * north_star).  d_ws: b64_batch_workspace_bytes(k, total_in, 0) bytes,
+ * and each encoding contiguously to d_out.  Messages are cut into warp
+ * work units that never straddle messages, and every warp takes an equal
+ * contiguous range of units -- messages are assigned to warps by the prefix
+ * sums of their lengths (BASELINE.json north_star).  d_ws: b64_batch_workspace_bytes(k, total_in, 0) bytes,
  * total_in >= d_in_off[k] - d_in_off[0].  Asynchronous. */
 int b64_encode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
                      uint8_t *d_out, int64_t *d_out_off, void *d_ws, size_t ws_bytes,
@@ -232,14 +278,26 @@ int b64_decode_ws(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int
 /* End-to-end helpers with HOST buffers (pinned memory recommended): the
  * input is copied host->device in chunks, each chunk is processed as soon as
  * it lands and its output copied back, so transfers overlap the kernels.
- * d_scratch_in / d_scratch_out are device buffers of at least
- * n (resp. m) and b64_encoded_len(n) (resp. b64_decoded_max_len(m)) bytes.
- * Both synchronize `stream` before returning. */
+ * d_scratch_in / d_scratch_out are device buffers of at least n (resp. m)
+ * and b64_encoded_len_ex(n, flags) (resp. b64_decoded_max_len_ex(m, flags))
+ * bytes; h_out has the same capacity as d_scratch_out.  The copies run on
+ * internal streams that first wait for the work already queued on `stream`,
+ * so earlier kernels using the scratch buffers are not overtaken.  Decode
+ * chunks are shards (b64_decode_shard_ex_async) combined like the
+ * multi-GPU exchange (b64_combine_shards): status, err_pos and out_len are
+ * those of b64_decode_ex on the whole input.  Both synchronize `stream`
+ * before returning (also on failure, after draining the internal copies).
+ * The plain forms are the _ex forms with flags = 0. */
 int64_t b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, uint8_t *d_scratch_in,
                         uint8_t *d_scratch_out, b64_stream_t stream);
 int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out_len,
                     int64_t *err_pos, uint8_t *d_scratch_in, uint8_t *d_scratch_out,
                     b64_stream_t stream);
+int64_t b64_encode_host_ex(const uint8_t *h_in, int64_t n, uint8_t *h_out, int flags,
+                           uint8_t *d_scratch_in, uint8_t *d_scratch_out, b64_stream_t stream);
+int b64_decode_host_ex(const uint8_t *h_in, int64_t m, uint8_t *h_out, int flags, int64_t *out_len,
+                       int64_t *err_pos, uint8_t *d_scratch_in, uint8_t *d_scratch_out,
+                       b64_stream_t stream);
 
 /* ------------------------------------------------------------------ misc */
 

@@ -46,6 +46,11 @@ from ._lib import (  # noqa: F401
     b64_encode_host,
     b64_encoded_len,
     b64_shard,
+    b64_shard_key,
+    b64_combine_shards,
+    b64_combine_shards_async,
+    b64_decode_shard_ex_async,
+    INT64_MAX,
     b64_status_str,
     lib_path,
     load_library,

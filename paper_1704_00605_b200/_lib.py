@@ -36,7 +36,10 @@ EXPORTS = (
     "b64_despace_workspace_bytes", "b64_despace",
     "b64_decode_ws_workspace_bytes", "b64_decode_ws", "b64_decode_ws_async",
     "b64_encoded_len_wrapped", "b64_encode_wrapped",
+    "b64_decode_shard_ex_async", "b64_shard_key", "b64_combine_shards", "b64_combine_shards_async",
+    "b64_encode_host_ex", "b64_decode_host_ex",
 )
+INT64_MAX = (1 << 63) - 1
 
 _lib = None
 
@@ -97,6 +100,12 @@ def load_library():
         "b64_decode_ws_async": (i32, [vp, i64, vp, i32, vp, vp, sz, vp]),
         "b64_decode_ws": (i32, [vp, i64, vp, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), vp, sz,
                                 vp]),
+        "b64_decode_shard_ex_async": (i32, [vp, i64, i64, i32, vp, i32, vp, vp, vp]),
+        "b64_shard_key": (i64, [ctypes.c_int32, i64, i64]),
+        "b64_combine_shards": (i32, [i64, vp, i32, i64, ctypes.POINTER(_Result)]),
+        "b64_combine_shards_async": (i32, [vp, vp, i32, i64, vp, vp]),
+        "b64_encode_host_ex": (i64, [vp, i64, vp, i32, vp, vp, vp]),
+        "b64_decode_host_ex": (i32, [vp, i64, vp, i32, p64, p64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -223,41 +232,113 @@ def unpack_result(res):
     return v[0], v[1], st, pc
 
 
+def _check_result(result):
+    import torch
+
+    if not (isinstance(result, torch.Tensor) and result.is_cuda and result.dtype == torch.int64
+            and result.is_contiguous() and result.numel() >= 3):
+        raise TypeError("result must be a contiguous int64[3] CUDA tensor")
+
+
+def _check_dec_args(inp, out, result, flags):
+    _check_u8_cuda(inp, "inp")
+    _check_u8_cuda(out, "out")
+    _check_result(result)
+    cap = load_library().b64_decoded_max_len_ex(inp.numel(), flags)
+    if cap < 0:
+        raise B64Error(B64_ERR_ARG, "flags")
+    if out.numel() < cap:
+        raise ValueError("out too small")
+
+
 def b64_decode_async(inp, out, result, stream=None, flags: int = 0):
-    if flags:
-        return b64_decode_ex_async(inp, out, result, flags, stream)
-    return b64_decode_shard_async(inp, out, result, final_shard=True, stream=stream)
+    """Asynchronous validating decode; the b64_result record lands in
+    ``result`` (int64[3] CUDA tensor, see unpack_result)."""
+    b64_decode_ex_async(inp, out, result, flags, stream)
 
 
 def b64_decode_ex_async(inp, out, result, flags: int, stream=None):
-    lib = load_library()
-    rc = lib.b64_decode_ex_async(_ptr(inp), inp.numel(), _ptr(out), flags, result.data_ptr(),
-                                 _stream(stream, inp.device))
+    _check_dec_args(inp, out, result, flags)
+    rc = load_library().b64_decode_ex_async(_ptr(inp), inp.numel(), _ptr(out), flags,
+                                            result.data_ptr(), _stream(stream, inp.device))
     if rc < 0:
         raise B64Error(rc, "b64_decode_ex_async")
 
 
 def b64_decode_shard_async(inp, out, result, final_shard=True, stream=None):
-    import torch
-
-    _check_u8_cuda(inp, "inp")
-    _check_u8_cuda(out, "out")
-    if not (result.is_cuda and result.dtype == torch.int64 and result.numel() >= 3):
-        raise TypeError("result must be an int64[3] CUDA tensor")
-    lib = load_library()
-    m = inp.numel()
-    if out.numel() < lib.b64_decoded_max_len(m):
-        raise ValueError("out too small")
-    rc = lib.b64_decode_shard_async(_ptr(inp), m, 1 if final_shard else 0, _ptr(out),
-                                    result.data_ptr(), _stream(stream, inp.device))
+    _check_dec_args(inp, out, result, 0)
+    rc = load_library().b64_decode_shard_async(_ptr(inp), inp.numel(), 1 if final_shard else 0,
+                                               _ptr(out), result.data_ptr(),
+                                               _stream(stream, inp.device))
     if rc < 0:
         raise B64Error(rc, "b64_decode_shard_async")
+
+
+def b64_decode_shard_ex_async(inp, out, result, shard_begin: int, final_shard: bool, flags: int = 0,
+                              key=None, stream=None):
+    """Shard decode with variant flags; ``key`` (int64[2] CUDA tensor or
+    None) receives (b64_shard_key, out_len) for the multi-GPU exchange."""
+    import torch
+
+    _check_dec_args(inp, out, result, flags)
+    if key is not None and not (isinstance(key, torch.Tensor) and key.is_cuda and
+                                key.dtype == torch.int64 and key.is_contiguous() and key.numel() >= 2):
+        raise TypeError("key must be a contiguous int64[2] CUDA tensor")
+    rc = load_library().b64_decode_shard_ex_async(
+        _ptr(inp), inp.numel(), shard_begin, 1 if final_shard else 0, _ptr(out), flags,
+        result.data_ptr(), _ptr(key), _stream(stream, inp.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_decode_shard_ex_async")
+
+
+def b64_shard_key(status: int, err_pos: int, shard_begin: int) -> int:
+    """Reduction key of one shard result (C ABI b64_shard_key, pure host)."""
+    return load_library().b64_shard_key(status, err_pos, shard_begin)
+
+
+def b64_combine_shards(key_min: int, shard_out_lens, total_m: int):
+    """(status, err_pos, out_len, pad_count) of the whole buffer from the MIN
+    reduction key and the shard output lengths (C ABI, pure host)."""
+    import numpy as np
+
+    lens = np.ascontiguousarray(np.asarray(shard_out_lens, dtype=np.int64))
+    r = _Result()
+    rc = load_library().b64_combine_shards(key_min, lens.ctypes.data, lens.size, total_m,
+                                           ctypes.byref(r))
+    if rc < 0:
+        raise B64Error(rc, "b64_combine_shards")
+    return r.status, r.err_pos, r.out_len, r.pad_count
+
+
+def b64_combine_shards_async(key_min, shard_out_lens, total_m: int, result, stream=None):
+    """Device form: key_min (int64[1]) and shard_out_lens (int64[world]) are
+    CUDA tensors; the record lands in ``result`` without a host sync."""
+    import torch
+
+    for t, nm in ((key_min, "key_min"), (shard_out_lens, "shard_out_lens")):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int64 and t.is_contiguous()):
+            raise TypeError(f"{nm} must be a contiguous int64 CUDA tensor")
+    _check_result(result)
+    rc = load_library().b64_combine_shards_async(key_min.data_ptr(), shard_out_lens.data_ptr(),
+                                                 shard_out_lens.numel(), total_m, result.data_ptr(),
+                                                 _stream(stream, result.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_combine_shards_async")
 
 
 # ------------------------------------------------------------- batched ---
 
 def b64_batch_workspace_bytes(k: int, total_in: int, direction: int) -> int:
     return load_library().b64_batch_workspace_bytes(k, total_in, direction)
+
+
+def _check_off(t, name, n=None):
+    import torch
+
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int64 and t.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous int64 CUDA tensor")
+    if n is not None and t.numel() < n:
+        raise ValueError(f"{name} too small")
 
 
 def _ws(k, total, direction, device, ws):
@@ -281,8 +362,16 @@ def b64_encode_batch(inp, in_off, out=None, out_off=None, ws=None, total_in=None
     total = inp.numel() if total_in is None else total_in
     if out is None:
         out = torch.empty(max(4 * ((total + 2) // 3) + 4 * k, 1), dtype=torch.uint8, device=inp.device)
+    else:
+        # the exact need (sum of per-message encoded lengths) lives on the
+        # device; every batch needs at least the whole-input encoded length
+        _check_u8_cuda(out, "out")
+        if out.numel() < (4 * total + 2) // 3:
+            raise ValueError("out too small")
+    _check_off(in_off, "in_off")
     if out_off is None:
         out_off = torch.empty(k + 1, dtype=torch.int64, device=inp.device)
+    _check_off(out_off, "out_off", k + 1)
     w, need = _ws(k, total, 0, inp.device, ws)
     rc = load_library().b64_encode_batch_ex(_ptr(inp), in_off.data_ptr(), k, total, _ptr(out),
                                             out_off.data_ptr(), flags, w.data_ptr(), w.numel(),
@@ -303,6 +392,9 @@ def b64_decode_batch(inp, in_off, out=None, out_off=None, out_len=None, err_pos=
     total = inp.numel() if total_in is None else total_in
     if out is None:
         out = torch.empty(max(3 * (total // 4) + 2 * k + 1, 1), dtype=torch.uint8, device=dev)
+    else:
+        _check_u8_cuda(out, "out")
+    _check_off(in_off, "in_off")
     if out_off is None:
         out_off = torch.empty(k + 1, dtype=torch.int64, device=dev)
     if out_len is None:
@@ -311,6 +403,11 @@ def b64_decode_batch(inp, in_off, out=None, out_off=None, out_len=None, err_pos=
         err_pos = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
     if status is None:
         status = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    _check_off(out_off, "out_off", k + 1)
+    _check_off(out_len, "out_len", k)
+    _check_off(err_pos, "err_pos", k)
+    if not (status.is_cuda and status.dtype == torch.int32 and status.is_contiguous() and status.numel() >= k):
+        raise TypeError("status must be a contiguous int32[k] CUDA tensor")
     w, need = _ws(k, total, 1, dev, ws)
     rc = load_library().b64_decode_batch_ex(_ptr(inp), in_off.data_ptr(), k, total, _ptr(out),
                                             out_off.data_ptr(), out_len.data_ptr(),
@@ -323,25 +420,49 @@ def b64_decode_batch(inp, in_off, out=None, out_off=None, out_len=None, err_pos=
 
 # -------------------------------------------------------- host buffers ---
 
-def b64_encode_host(h_in, h_out, d_scratch_in, d_scratch_out, stream=None):
+def _check_host(h, name, need):
+    import torch
+
+    if not (isinstance(h, torch.Tensor) and h.dtype == torch.uint8 and not h.is_cuda and h.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous uint8 CPU tensor")
+    if h.numel() < need:
+        raise ValueError(f"{name} too small")
+
+
+def b64_encode_host(h_in, h_out, d_scratch_in, d_scratch_out, stream=None, flags: int = 0):
     """h_in/h_out: (pinned) CPU uint8 tensors; returns the output length."""
     lib = load_library()
     n = h_in.numel()
-    rc = lib.b64_encode_host(_ptr(h_in), n, _ptr(h_out), _ptr(d_scratch_in), _ptr(d_scratch_out),
-                             _stream(stream, d_scratch_in.device))
+    need = lib.b64_encoded_len_ex(n, flags)
+    _check_host(h_in, "h_in", n)
+    _check_host(h_out, "h_out", need)
+    _check_u8_cuda(d_scratch_in, "d_scratch_in")
+    _check_u8_cuda(d_scratch_out, "d_scratch_out")
+    if d_scratch_in.numel() < n or d_scratch_out.numel() < need:
+        raise ValueError("scratch too small")
+    rc = lib.b64_encode_host_ex(_ptr(h_in), n, _ptr(h_out), flags, _ptr(d_scratch_in),
+                                _ptr(d_scratch_out), _stream(stream, d_scratch_in.device))
     if rc < 0:
         raise B64Error(rc, "b64_encode_host")
     return rc
 
 
-def b64_decode_host(h_in, h_out, d_scratch_in, d_scratch_out, stream=None):
+def b64_decode_host(h_in, h_out, d_scratch_in, d_scratch_out, stream=None, flags: int = 0):
     """Returns (status, out_len, err_pos)."""
     lib = load_library()
+    m = h_in.numel()
+    cap = lib.b64_decoded_max_len_ex(m, flags)
+    _check_host(h_in, "h_in", m)
+    _check_host(h_out, "h_out", cap)
+    _check_u8_cuda(d_scratch_in, "d_scratch_in")
+    _check_u8_cuda(d_scratch_out, "d_scratch_out")
+    if d_scratch_in.numel() < m or d_scratch_out.numel() < cap:
+        raise ValueError("scratch too small")
     ol = ctypes.c_int64(0)
     ep = ctypes.c_int64(0)
-    st = lib.b64_decode_host(_ptr(h_in), h_in.numel(), _ptr(h_out), ctypes.byref(ol),
-                             ctypes.byref(ep), _ptr(d_scratch_in), _ptr(d_scratch_out),
-                             _stream(stream, d_scratch_in.device))
+    st = lib.b64_decode_host_ex(_ptr(h_in), m, _ptr(h_out), flags, ctypes.byref(ol),
+                                ctypes.byref(ep), _ptr(d_scratch_in), _ptr(d_scratch_out),
+                                _stream(stream, d_scratch_in.device))
     if st < 0:
         raise B64Error(st, "b64_decode_host")
     return st, ol.value, ep.value
@@ -385,6 +506,10 @@ def b64_despace(inp, out=None, ws=None, stream=None):
     m = inp.numel()
     if out is None:
         out = torch.empty(max(m, 1), dtype=torch.uint8, device=inp.device)
+    else:
+        _check_u8_cuda(out, "out")
+        if out.numel() < m:
+            raise ValueError("out too small")
     need = lib.b64_despace_workspace_bytes(m)
     if ws is None or ws.numel() < need:
         ws = torch.empty(max(need, 256), dtype=torch.uint8, device=inp.device)

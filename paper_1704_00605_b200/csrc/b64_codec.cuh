@@ -5,6 +5,8 @@
 #pragma once
 #include <cstdint>
 
+#include "b64_knobs.cuh"  // measurement-only knobs (never set in the product build)
+
 namespace b64 {
 
 // ------------------------------------------------------------ geometry ---
@@ -28,9 +30,6 @@ namespace b64 {
 #ifndef B64_BATCH_SLOTS   // per-warp input ring depth (batched)
 #define B64_BATCH_SLOTS 2
 #endif
-#ifndef B64_BATCH_PREFETCH  // batched: L2 prefetch distance in units (0 = off)
-#define B64_BATCH_PREFETCH 0
-#endif
 #ifndef B64_BATCH_CTAS    // batched: CTAs per SM of the cooperative grid
 #define B64_BATCH_CTAS 1
 #endif
@@ -39,15 +38,6 @@ namespace b64 {
 #endif
 #ifndef B64_CTAS_PER_SM
 #define B64_CTAS_PER_SM 1
-#endif
-#ifndef B64_SKELETON  // measurement only: move the bytes, skip the transform
-#define B64_SKELETON 0
-#endif
-#ifndef B64_ENC_ARITH  // measurement only: Table I mapping by SWAR arithmetic instead of the table
-#define B64_ENC_ARITH 0
-#endif
-#ifndef B64_DEC_STG64  // with B64_DEC_STG32: one 8-byte + one 4-byte store per 12-byte run
-#define B64_DEC_STG64 0
 #endif
 #ifndef B64_DEC_STG32  // decode DIRECT tiles: three 4-byte stores from registers (no smem slice)
 #define B64_DEC_STG32 1
@@ -65,7 +55,8 @@ static_assert(kStagesOut >= 2, "output staging needs >= 2 slots");
 
 // Encode: each compute thread turns 12 bytes (4 groups) into 16 chars per
 // pass; decode: 16 chars (4 quads) into 12 bytes per pass.  A tile is P
-// passes of the 256 compute threads.
+// passes of the kNT compute threads (512 at the default 16 warps: with
+// P = 4, encode tiles are 24 KiB in / 32 KiB out, decode 32 KiB / 24 KiB).
 template <int P>
 struct EncG {
   static constexpr int kPasses = P;
@@ -78,7 +69,7 @@ struct DecG {
   static constexpr int kIn = kNT * 16 * P;   // input chars per tile
   static constexpr int kOut = kNT * 12 * P;  // output bytes per tile
 };
-constexpr int kSinglePasses = B64_SINGLE_PASSES;  // single buffer: 12 KiB in / 16 KiB out (encode)
+constexpr int kSinglePasses = B64_SINGLE_PASSES;  // single-buffer tile = this many passes
 constexpr int kBatchPasses = B64_BATCH_PASSES;    // batched: one warp unit = this many passes
 
 constexpr int round_up_c(int x, int a) { return (x + a - 1) / a * a; }

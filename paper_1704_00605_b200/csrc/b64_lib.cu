@@ -1,13 +1,16 @@
 // b64_lib.cu -- sm_100a kernels and the C ABI of libb64gpu.so (include/b64gpu.h).
 //
-// Kernel structure:
-//   persistent grid (2 CTAs per SM); per CTA 8 compute warps + 1 producer
-//   warp.  The producer lane streams input tiles HBM -> smem with 1-D bulk
-//   (TMA) copies into a 4-stage mbarrier ring; compute warps transform the
-//   tile smem -> smem; one elected thread writes the output tile smem -> HBM
-//   with a bulk copy (plus byte stores for the <16-byte unaligned edges).
-//   Every HBM access is thus a 16-byte-granular bulk transfer, although
-//   3-byte groups and 4-char quads do not align to 16 B.
+// Single-buffer kernel structure (defaults in b64_codec.cuh):
+//   persistent grid of B64_CTAS_PER_SM (1) CTA per SM; per CTA B64_WARPS_C
+//   (16) compute warps + 1 producer warp.  The producer lane streams input
+//   tiles HBM -> smem with 1-D bulk (TMA) copies into a B64_STAGES_IN (3)
+//   stage full/empty mbarrier ring.  Compute warps transform their slice of
+//   the tile in registers; full tiles with a 16-byte aligned destination are
+//   stored straight from registers (encode: one STG.128 per thread, decode:
+//   three STG.32), other tiles are staged in smem and leave through one bulk
+//   store (plus byte stores for the < 16-byte unaligned edges).  Every HBM
+//   access is thus a 16-byte-granular transfer, although 3-byte groups and
+//   4-char quads do not align to 16 B.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -26,6 +29,14 @@
 #include "b64_ws.cuh"
 #include "b64_wrap.cuh"
 #include "b64_wslines.cuh"
+#include "b64_onepass.cuh"
+
+// f3 / f4 general path: single-read kernels (b64_onepass.cuh) or the
+// two-pass mask + compaction kernels (b64_compact.cuh, b64_ws.cuh; kept for
+// A/B measurement only).
+#ifndef B64_CP_ONEPASS
+#define B64_CP_ONEPASS 0
+#endif
 
 namespace b64 {
 
@@ -61,6 +72,49 @@ struct DecWs {                 // per-(device, stream) decode scratch (self-rese
   unsigned int done;           // CTAs finished
   unsigned int pad;
 };
+
+// ------------------------------------------- multi-GPU result exchange ---
+// the shards of one buffer are decoded independently; the
+// only exchange is one MIN all-reduce and one length all-gather.  A shard's
+// reduction key packs its first error as a GLOBAL offset together with its
+// status, (begin + err_pos) * 4 + status, or INT64_MAX when the shard is
+// clean.  Shards cover disjoint offsets, so the MIN over shards is the first
+// error of the whole buffer (the first offending byte) and carries
+// that shard's status -- INVALID_CHAR, LENGTH (last shard only) or
+// NONCANONICAL (last shard, B64_FLAG_STRICT) -- which err_pos alone does not
+// determine once variant flags are on.
+__host__ __device__ inline int64_t shard_key(int32_t status, int64_t err_pos, int64_t begin) {
+  return status == 0 ? static_cast<int64_t>(LLONG_MAX) : (begin + err_pos) * 4 + status;
+}
+
+// Whole-buffer result from the reduced key and the per-shard output lengths.
+// On any error out_len = 3*floor(err_pos/4): Alg 2 appends nothing for the
+// failing quad, and LENGTH (err_pos = 4*floor(m/4)) and the
+// variant errors of the final quad follow the same rule (b64_decode).  A
+// clean buffer's length is the sum of the shard lengths.
+__host__ __device__ inline b64_result combine_shards(int64_t key_min, const int64_t *lens, int world,
+                                                     int64_t total_m) {
+  b64_result R;
+  if (key_min == static_cast<int64_t>(LLONG_MAX)) {
+    int64_t t = 0;
+    for (int r = 0; r < world; ++r) t += lens[r];
+    R.out_len = t;
+    R.err_pos = -1;
+    R.status = 0;
+    R.pad_count = (total_m % 4 == 0) ? static_cast<int32_t>(3 * (total_m / 4) - t) : 0;
+  } else {
+    R.err_pos = key_min >> 2;
+    R.status = static_cast<int32_t>(key_min & 3);
+    R.out_len = 3 * (R.err_pos / 4);
+    R.pad_count = 0;
+  }
+  return R;
+}
+
+__global__ void combine_kernel(const int64_t *key_min, const int64_t *lens, int world,
+                               int64_t total_m, b64_result *out) {
+  if (threadIdx.x == 0) *out = combine_shards(*key_min, lens, world, total_m);
+}
 
 // ------------------------------------------------- tile descriptors ---
 template <int P>
@@ -209,7 +263,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 template <int IA, int OA, int P = kSinglePasses>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
-                  int64_t ntiles, int final_shard, DecWs *ws, b64_result *res, int flags) {
+                  int64_t ntiles, int final_shard, DecWs *ws, b64_result *res, int flags,
+                  int64_t shard_begin, int64_t *key) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using G = DecG<P>;
   DecSmemP<P> &S = *reinterpret_cast<DecSmemP<P> *>(smem_raw);
@@ -298,6 +353,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       res->err_pos = R.err_pos;
       res->status = R.status;
       res->pad_count = R.pad_count;
+      if (key != nullptr) {
+        // Multi-GPU exchange record (include/b64gpu.h b64_decode_shard_ex_async)
+        key[0] = shard_key(R.status, R.err_pos, shard_begin);
+        key[1] = R.out_len;
+      }
       ws->errkey = ~0ull;
       ws->done = 0;
       // (no system-scope fence: kernel completion makes these writes --
@@ -318,9 +378,9 @@ using namespace b64;
 struct DevInfo {
   int sms = 0;
   int wl_ctas = 1;  // resident decode_lines_kernel CTAs per SM
+  int op_ctas = 1;   // resident one-pass compaction CTAs per SM
   bool attrs_set = false;
 };
-int g_wl_ctas = 1;
 
 std::mutex g_mu;
 std::map<int, DevInfo> g_dev;
@@ -337,7 +397,7 @@ struct StreamWs {
   // host-buffer pipeline (created on first use)
   bool pipe = false;
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t e_in = nullptr, e_comp = nullptr, e_done = nullptr;
+  cudaEvent_t e_in = nullptr, e_comp = nullptr, e_done = nullptr, e_entry = nullptr;
   b64_result *h_chunks = nullptr, *d_chunks = nullptr;  // mapped, kMaxHostChunks records
 };
 std::map<std::pair<int, uintptr_t>, StreamWs> g_ws;
@@ -351,7 +411,8 @@ cudaError_t set_smem(K kernel, int bytes) {
 
 // Kernel tables indexed by alignment class (0: 16-aligned, 1: 4-aligned, 2: unaligned).
 using EncFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int);
-using DecFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int, DecWs *, b64_result *, int);
+using DecFn = void (*)(const uint8_t *, int64_t, uint8_t *, int64_t, int, DecWs *, b64_result *, int,
+                      int64_t, int64_t *);
 
 EncFn enc_table[3][3] = {
     {encode_kernel<16, 16>, encode_kernel<16, 4>, encode_kernel<16, 1>},
@@ -383,45 +444,83 @@ int align_class(const void *p) {
 }
 
 // Device info + one-time kernel attributes.
-bool device_setup(int *dev_out, int *sms_out) {
+DevInfo *device_setup_info(int *dev_out) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lk(g_mu);
   DevInfo &di = g_dev[dev];
   if (!di.attrs_set) {
     if (cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      return false;
+      return nullptr;
     for (auto &row : enc_table)
       for (auto f : row)
-        if (set_smem(f, sizeof(EncSmem)) != cudaSuccess) return false;
+        if (set_smem(f, sizeof(EncSmem)) != cudaSuccess) return nullptr;
     for (auto &row : dec_table)
       for (auto f : row)
-        if (set_smem(f, sizeof(DecSmem)) != cudaSuccess) return false;
+        if (set_smem(f, sizeof(DecSmem)) != cudaSuccess) return nullptr;
     for (auto &row : enc_small_table)
       for (auto f : row)
-        if (set_smem(f, sizeof(EncSmemP<kSmallPasses>)) != cudaSuccess) return false;
+        if (set_smem(f, sizeof(EncSmemP<kSmallPasses>)) != cudaSuccess) return nullptr;
     for (auto &row : dec_small_table)
       for (auto f : row)
-        if (set_smem(f, sizeof(DecSmemP<kSmallPasses>)) != cudaSuccess) return false;
-    if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return false;
-    if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return false;
-    if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return false;
-    if (set_smem(decode_lines_kernel, sizeof(WlSmem)) != cudaSuccess) return false;
+        if (set_smem(f, sizeof(DecSmemP<kSmallPasses>)) != cudaSuccess) return nullptr;
+    if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return nullptr;
+    if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(decode_lines_kernel, sizeof(WlSmem)) != cudaSuccess) return nullptr;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.wl_ctas, decode_lines_kernel, kWlThreads,
                                                       sizeof(WlSmem)) != cudaSuccess ||
         di.wl_ctas < 1)
       di.wl_ctas = 1;
-    g_wl_ctas = di.wl_ctas;
-    if (set_smem(encode_wrap_kernel<2, true>, sizeof(WrSmem)) != cudaSuccess) return false;
-    if (set_smem(encode_wrap_kernel<2, false>, sizeof(WrSmem)) != cudaSuccess) return false;
-    if (set_smem(encode_wrap_kernel<1, false>, sizeof(WrSmem)) != cudaSuccess) return false;
-    if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return false;
+    if (set_smem(encode_wrap_kernel<2, true>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(encode_wrap_kernel<2, false>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(encode_wrap_kernel<1, false>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
+    if (set_smem(despace1_kernel, sizeof(OpDsSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(decode_ws1_kernel, sizeof(OpWsSmem)) != cudaSuccess) return nullptr;
+    int o1 = 0, o2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, despace1_kernel, kOpThreads,
+                                                      sizeof(OpDsSmem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, decode_ws1_kernel, kOpThreads,
+                                                      sizeof(OpWsSmem)) != cudaSuccess)
+      return nullptr;
+    di.op_ctas = o1 < o2 ? o1 : o2;
+    if (di.op_ctas < 1) return nullptr;
     di.attrs_set = true;
   }
   *dev_out = dev;
-  *sms_out = di.sms;
+  return &di;
+}
+
+bool device_setup(int *dev_out, int *sms_out) {
+  DevInfo *di = device_setup_info(dev_out);
+  if (di == nullptr) return false;
+  *sms_out = di->sms;
   return true;
 }
+
+// Every launching entry point runs on the device that owns `stream` (a
+// caller's cuda:1 stream works while the thread's current device is 0, as
+// with torch ops); the legacy / per-thread default streams use the current
+// device.  The previous current device is restored on return.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(cudaStream_t s) {
+    if (s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread) return;
+    // during stream capture the capturing thread's device is already the
+    // stream's, and device queries on a capturing stream invalidate it
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    int d = 0, cur = 0;
+    if (cudaStreamGetDevice(s, &d) != cudaSuccess || cudaGetDevice(&cur) != cudaSuccess) return;
+    if (d != cur && cudaSetDevice(d) == cudaSuccess) prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+
 
 StreamWs *stream_ws(int dev, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -443,7 +542,7 @@ bool pipe_setup(StreamWs *w) {
   if (w->pipe) return true;
   if (cudaStreamCreateWithFlags(&w->s_in, cudaStreamNonBlocking) != cudaSuccess) return false;
   if (cudaStreamCreateWithFlags(&w->s_out, cudaStreamNonBlocking) != cudaSuccess) return false;
-  for (cudaEvent_t *e : {&w->e_in, &w->e_comp, &w->e_done})
+  for (cudaEvent_t *e : {&w->e_in, &w->e_comp, &w->e_done, &w->e_entry})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return false;
   if (cudaHostAlloc(&w->h_chunks, kMaxHostChunks * sizeof(b64_result), cudaHostAllocMapped) !=
       cudaSuccess)
@@ -462,6 +561,18 @@ int64_t host_chunk(int64_t total, int64_t base, int64_t unit) {
   return c;
 }
 
+bool pipe_enter(StreamWs *w, cudaStream_t stream) {
+  return cudaEventRecord(w->e_entry, stream) == cudaSuccess &&
+         cudaStreamWaitEvent(w->s_in, w->e_entry, 0) == cudaSuccess &&
+         cudaStreamWaitEvent(w->s_out, w->e_entry, 0) == cudaSuccess;
+}
+template <class T>
+T pipe_fail(StreamWs *w, T rc) {
+  cudaStreamSynchronize(w->s_in);
+  cudaStreamSynchronize(w->s_out);
+  return rc;
+}
+
 int64_t grid_for(int64_t ntiles, int sms) {
   int64_t g = static_cast<int64_t>(sms) * ctas_per_sm();
   if (ntiles < g) g = ntiles;
@@ -469,7 +580,8 @@ int64_t grid_for(int64_t ntiles, int sms) {
 }
 
 int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
-                  b64_result *d_result, cudaStream_t stream, DecWs *ws, int flags = 0) {
+                  b64_result *d_result, cudaStream_t stream, DecWs *ws, int flags = 0,
+                  int64_t shard_begin = 0, int64_t *d_key = nullptr) {
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   const int64_t chars = 4 * (m / 4);
@@ -480,7 +592,7 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
   DecFn f = (small ? dec_small_table : dec_table)[align_class(d_in)][align_class(d_out)];
   const size_t smem = small ? sizeof(DecSmemP<kSmallPasses>) : sizeof(DecSmem);
   f<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(d_in, m, d_out, ntiles, final_shard, ws,
-                                                             d_result, flags);
+                                                             d_result, flags, shard_begin, d_key);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
@@ -495,6 +607,25 @@ size_t ws_layout(int64_t k, size_t *off_units, size_t *off_done) {
   *off_done = o;  // first_msg[grid * kBWarps] (int32): each warp's first message
   o += static_cast<size_t>(kMaxBatchCtas) * kBWarps * sizeof(int32_t);
   return (o + 255) & ~static_cast<size_t>(255);
+}
+
+int64_t op_ntiles(const void *d_in, int64_t m) {
+  const int64_t imis = static_cast<int64_t>(reinterpret_cast<uintptr_t>(d_in) & 15);
+  return (imis + m + kCpTile - 1) / kCpTile;
+}
+
+// Cooperative launch of a one-pass compaction kernel: its prefix waits on
+// other CTAs, so every CTA of the grid must be resident.
+template <class... A>
+int op_launch(void (*k)(A...), int64_t ntiles, const DevInfo *di, size_t smem,
+                     cudaStream_t stream, A... args) {
+  int64_t g = static_cast<int64_t>(di->sms) * di->op_ctas;
+  if (g > ntiles) g = ntiles;
+  void *argv[] = {&args...};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(k), dim3(static_cast<unsigned>(g)),
+                                     dim3(kOpThreads), argv, smem, stream) == cudaSuccess
+             ? B64_OK
+             : B64_ERR_CUDA;
 }
 
 }  // namespace
@@ -525,6 +656,7 @@ int64_t b64_encode_ex(const uint8_t *d_in, int64_t n, uint8_t *d_out, int flags,
   if (n < 0 || !flags_ok(flags) || (n > 0 && (d_in == nullptr || d_out == nullptr)))
     return B64_ERR_ARG;
   if (n == 0) return 0;
+  DevGuard g(stream);
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   int64_t ntiles = (n + EncS1::kIn - 1) / EncS1::kIn;
@@ -543,21 +675,52 @@ int64_t b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, b64_stream_t 
 }
 
 static int decode_shard_ex(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
-                           int flags, b64_result *d_result, cudaStream_t stream) {
+                           int flags, b64_result *d_result, cudaStream_t stream,
+                           int64_t shard_begin = 0, int64_t *d_key = nullptr) {
   if (m < 0 || !flags_ok(flags) || d_result == nullptr || (m > 0 && d_in == nullptr) ||
-      (b64_decoded_max_len_ex(m, flags) > 0 && d_out == nullptr))
+      (b64_decoded_max_len_ex(m, flags) > 0 && d_out == nullptr) || shard_begin < 0)
     return B64_ERR_ARG;
   if (!final_shard && (m % 4) != 0) return B64_ERR_ARG;
+  DevGuard g(stream);
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
   if (w == nullptr) return B64_ERR_CUDA;
-  return decode_launch(d_in, m, final_shard, d_out, d_result, stream, w->d_ws, flags);
+  return decode_launch(d_in, m, final_shard, d_out, d_result, stream, w->d_ws, flags, shard_begin,
+                       d_key);
 }
 
 int b64_decode_shard_async(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_out,
                            b64_result *d_result, b64_stream_t stream) {
   return decode_shard_ex(d_in, m, final_shard, d_out, 0, d_result, stream);
+}
+
+int b64_decode_shard_ex_async(const uint8_t *d_in, int64_t m, int64_t shard_begin, int final_shard,
+                              uint8_t *d_out, int flags, b64_result *d_result, int64_t *d_key,
+                              b64_stream_t stream) {
+  return decode_shard_ex(d_in, m, final_shard, d_out, flags, d_result, stream, shard_begin, d_key);
+}
+
+int64_t b64_shard_key(int32_t status, int64_t err_pos, int64_t shard_begin) {
+  return shard_key(status, err_pos, shard_begin);
+}
+
+int b64_combine_shards(int64_t key_min, const int64_t *h_shard_out_len, int world, int64_t total_m,
+                       b64_result *h_result) {
+  if (world <= 0 || h_shard_out_len == nullptr || h_result == nullptr || total_m < 0 || key_min < 0)
+    return B64_ERR_ARG;
+  *h_result = combine_shards(key_min, h_shard_out_len, world, total_m);
+  return B64_OK;
+}
+
+int b64_combine_shards_async(const int64_t *d_key_min, const int64_t *d_shard_out_len, int world,
+                             int64_t total_m, b64_result *d_result, b64_stream_t stream) {
+  if (world <= 0 || d_key_min == nullptr || d_shard_out_len == nullptr || d_result == nullptr ||
+      total_m < 0)
+    return B64_ERR_ARG;
+  DevGuard g(stream);
+  combine_kernel<<<1, 32, 0, stream>>>(d_key_min, d_shard_out_len, world, total_m, d_result);
+  return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }
 
 int b64_decode_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, b64_result *d_result,
@@ -575,6 +738,7 @@ int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int
   if (m < 0 || !flags_ok(flags) || (m > 0 && d_in == nullptr) ||
       (b64_decoded_max_len_ex(m, flags) > 0 && d_out == nullptr))
     return B64_ERR_ARG;
+  DevGuard g(stream);
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
@@ -615,6 +779,7 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
   size_t off_units, off_done;
   const size_t need = ws_layout(k, &off_units, &off_done);
   if (ws_bytes < need) return B64_ERR_WORKSPACE;
+  DevGuard g(stream);
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   uint8_t *ws = static_cast<uint8_t *>(d_ws);
@@ -686,49 +851,69 @@ int b64_decode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, in
 // Host-buffer entry points: the input is split into chunks; chunk i is
 // copied in on an internal stream, processed on `stream` as soon as it lands
 // and copied out on a second internal stream, so H2D, kernels and D2H of
-// different chunks overlap (PCIe / C2C full duplex).
-int64_t b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, uint8_t *d_scratch_in,
-                        uint8_t *d_scratch_out, b64_stream_t stream) {
-  if (n < 0 || (n > 0 && (!h_in || !h_out || !d_scratch_in || !d_scratch_out))) return B64_ERR_ARG;
+// different chunks overlap (PCIe / C2C full duplex).  Both internal streams
+// first wait for the work already queued on `stream` (stream order: an
+// earlier kernel that still reads d_scratch_in / writes d_scratch_out is not
+// overtaken by the copies).  On a failure after the first copy was queued
+// the internal streams are drained before returning, so no DMA into caller
+// buffers is left in flight.
+
+int64_t b64_encode_host_ex(const uint8_t *h_in, int64_t n, uint8_t *h_out, int flags,
+                           uint8_t *d_scratch_in, uint8_t *d_scratch_out, b64_stream_t stream) {
+  if (n < 0 || !flags_ok(flags) || (n > 0 && (!h_in || !h_out || !d_scratch_in || !d_scratch_out)))
+    return B64_ERR_ARG;
   if (n == 0) return 0;
+  DevGuard g(stream);
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
   if (w == nullptr || !pipe_setup(w)) return B64_ERR_CUDA;
-  const int64_t C = host_chunk(n, int64_t(3 * B64_HOST_CHUNK_MB) << 20, 48);  // multiple of 3 and 16
+  if (!pipe_enter(w, stream)) return pipe_fail<int64_t>(w, B64_ERR_CUDA);
+  // chunks are whole groups (a multiple of 3 and 16): only the last one has a tail
+  const int64_t C = host_chunk(n, int64_t(3 * B64_HOST_CHUNK_MB) << 20, 48);
   for (int64_t off = 0; off < n; off += C) {
     const int64_t len = n - off < C ? n - off : C;
-    const int64_t ooff = off / 3 * 4, olen = 4 * ((len + 2) / 3);
+    const int64_t ooff = off / 3 * 4, olen = enc_len(len, flags);
     if (cudaMemcpyAsync(d_scratch_in + off, h_in + off, len, cudaMemcpyHostToDevice, w->s_in) !=
             cudaSuccess ||
         cudaEventRecord(w->e_in, w->s_in) != cudaSuccess ||
         cudaStreamWaitEvent(stream, w->e_in, 0) != cudaSuccess)
-      return B64_ERR_CUDA;
-    const int64_t rc = b64_encode(d_scratch_in + off, len, d_scratch_out + ooff, stream);
-    if (rc < 0) return rc;
+      return pipe_fail<int64_t>(w, B64_ERR_CUDA);
+    const int64_t rc = b64_encode_ex(d_scratch_in + off, len, d_scratch_out + ooff, flags, stream);
+    if (rc < 0) return pipe_fail(w, rc);
     if (cudaEventRecord(w->e_comp, stream) != cudaSuccess ||
         cudaStreamWaitEvent(w->s_out, w->e_comp, 0) != cudaSuccess ||
         cudaMemcpyAsync(h_out + ooff, d_scratch_out + ooff, olen, cudaMemcpyDeviceToHost, w->s_out) !=
             cudaSuccess)
-      return B64_ERR_CUDA;
+      return pipe_fail<int64_t>(w, B64_ERR_CUDA);
   }
   if (cudaEventRecord(w->e_done, w->s_out) != cudaSuccess ||
       cudaStreamWaitEvent(stream, w->e_done, 0) != cudaSuccess ||
       cudaStreamSynchronize(stream) != cudaSuccess)
-    return B64_ERR_CUDA;
-  return 4 * ((n + 2) / 3);
+    return pipe_fail<int64_t>(w, B64_ERR_CUDA);
+  return enc_len(n, flags);
 }
 
-int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out_len,
-                    int64_t *err_pos, uint8_t *d_scratch_in, uint8_t *d_scratch_out,
-                    b64_stream_t stream) {
-  if (m < 0 || (m > 0 && (!h_in || !d_scratch_in)) || (m >= 4 && (!h_out || !d_scratch_out)))
+int64_t b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, uint8_t *d_scratch_in,
+                        uint8_t *d_scratch_out, b64_stream_t stream) {
+  return b64_encode_host_ex(h_in, n, h_out, 0, d_scratch_in, d_scratch_out, stream);
+}
+
+int b64_decode_host_ex(const uint8_t *h_in, int64_t m, uint8_t *h_out, int flags, int64_t *out_len,
+                       int64_t *err_pos, uint8_t *d_scratch_in, uint8_t *d_scratch_out,
+                       b64_stream_t stream) {
+  if (m < 0 || !flags_ok(flags) || (m > 0 && (!h_in || !d_scratch_in)) ||
+      (b64_decoded_max_len_ex(m, flags) > 0 && (!h_out || !d_scratch_out)))
     return B64_ERR_ARG;
+  DevGuard g(stream);
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
   if (w == nullptr || !pipe_setup(w)) return B64_ERR_CUDA;
-  const int64_t C = host_chunk(m, int64_t(4 * B64_HOST_CHUNK_MB) << 20, 64);  // multiple of 4 and 16
+  if (!pipe_enter(w, stream)) return pipe_fail(w, static_cast<int>(B64_ERR_CUDA));
+  // chunks of whole quads (a multiple of 4 and 16), decoded as shards: only
+  // the last one applies the final-quad rules and the variant tail (R-shard)
+  const int64_t C = host_chunk(m, int64_t(4 * B64_HOST_CHUNK_MB) << 20, 64);
   int nch = 0;
   for (int64_t off = 0; off == 0 || off < m; off += C, ++nch) {
     const int64_t len = m - off < C ? m - off : C;
@@ -737,17 +922,17 @@ int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out
                                     w->s_in) != cudaSuccess ||
                     cudaEventRecord(w->e_in, w->s_in) != cudaSuccess ||
                     cudaStreamWaitEvent(stream, w->e_in, 0) != cudaSuccess))
-      return B64_ERR_CUDA;
+      return pipe_fail(w, static_cast<int>(B64_ERR_CUDA));
     const int64_t ooff = off / 4 * 3;
     const int rc = decode_launch(d_scratch_in + off, len, last ? 1 : 0, d_scratch_out + ooff,
-                                 w->d_chunks + nch, stream, w->d_ws);
-    if (rc != B64_OK) return rc;
-    const int64_t cap = 3 * (len / 4);
+                                 w->d_chunks + nch, stream, w->d_ws, flags);
+    if (rc != B64_OK) return pipe_fail(w, rc);
+    const int64_t cap = b64_decoded_max_len_ex(len, last ? flags : 0);
     if (cap > 0 && (cudaEventRecord(w->e_comp, stream) != cudaSuccess ||
                     cudaStreamWaitEvent(w->s_out, w->e_comp, 0) != cudaSuccess ||
                     cudaMemcpyAsync(h_out + ooff, d_scratch_out + ooff, cap,
                                     cudaMemcpyDeviceToHost, w->s_out) != cudaSuccess))
-      return B64_ERR_CUDA;
+      return pipe_fail(w, static_cast<int>(B64_ERR_CUDA));
     if (last) {
       ++nch;
       break;
@@ -756,25 +941,28 @@ int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out
   if (cudaEventRecord(w->e_done, w->s_out) != cudaSuccess ||
       cudaStreamWaitEvent(stream, w->e_done, 0) != cudaSuccess ||
       cudaStreamSynchronize(stream) != cudaSuccess)
-    return B64_ERR_CUDA;
-  // Combine the chunk records: the first chunk with an error decides
-  // (chunks split on 4-character boundaries, R-shard).
-  int64_t total = 0;
+    return pipe_fail(w, static_cast<int>(B64_ERR_CUDA));
+  // Combine the chunk records exactly as the multi-GPU exchange does: the
+  // minimum reduction key over the chunks, lengths summed when clean.
+  int64_t kmin = LLONG_MAX, lens[kMaxHostChunks];
   for (int i = 0; i < nch; ++i) {
     b64_result r;
     std::memcpy(&r, w->h_chunks + i, sizeof(r));
-    const int64_t off = static_cast<int64_t>(i) * C;
-    if (r.status != B64_OK) {
-      const int64_t e = off + r.err_pos;
-      if (out_len) *out_len = r.status == B64_ERR_LENGTH ? off / 4 * 3 + r.out_len : 3 * (e / 4);
-      if (err_pos) *err_pos = e;
-      return r.status;
-    }
-    total += r.out_len;
+    const int64_t k = shard_key(r.status, r.err_pos, static_cast<int64_t>(i) * C);
+    if (k < kmin) kmin = k;
+    lens[i] = r.out_len;
   }
-  if (out_len) *out_len = total;
-  if (err_pos) *err_pos = -1;
-  return B64_OK;
+  const b64_result R = combine_shards(kmin, lens, nch, m);
+  if (out_len) *out_len = R.out_len;
+  if (err_pos) *err_pos = R.err_pos;
+  return R.status;
+}
+
+int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, int64_t *out_len,
+                    int64_t *err_pos, uint8_t *d_scratch_in, uint8_t *d_scratch_out,
+                    b64_stream_t stream) {
+  return b64_decode_host_ex(h_in, m, h_out, 0, out_len, err_pos, d_scratch_in, d_scratch_out,
+                            stream);
 }
 
 // Chunking of the compaction kernels: one chunk of consecutive 16 KiB tiles
@@ -797,7 +985,11 @@ static size_t cp_mask_bytes(int64_t m) {
 
 size_t b64_despace_workspace_bytes(int64_t m) {
   if (m < 0) return 0;
+#if B64_CP_ONEPASS
+  return 4 * static_cast<size_t>((15 + m + kCpTile - 1) / kCpTile);  // per-tile kept counts
+#else
   return 8 * kCpMaxChunks + cp_mask_bytes(m);  // per-chunk kept counts + keep masks
+#endif
 }
 
 int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_len, void *d_ws,
@@ -807,13 +999,23 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
   if (m > 0 && (d_ws == nullptr || ws_bytes < b64_despace_workspace_bytes(m) ||
                  (reinterpret_cast<uintptr_t>(d_ws) & 15) != 0))
     return B64_ERR_WORKSPACE;
+  DevGuard g(stream);
   if (m == 0)
     return cudaMemsetAsync(d_out_len, 0, sizeof(int64_t), stream) == cudaSuccess ? B64_OK
                                                                                  : B64_ERR_CUDA;
-  int dev, sms;
-  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  int dev;
+  DevInfo *di = device_setup_info(&dev);
+  if (di == nullptr) return B64_ERR_CUDA;
+#if B64_CP_ONEPASS
+  const int64_t ntiles = op_ntiles(d_in, m);
+  uint32_t *cnt = static_cast<uint32_t *>(d_ws);
+  if (cudaMemsetAsync(cnt, 0, 4 * static_cast<size_t>(ntiles), stream) != cudaSuccess)
+    return B64_ERR_CUDA;
+  return op_launch(despace1_kernel, ntiles, di, sizeof(OpDsSmem), stream, d_in, m, d_out, cnt,
+                   d_out_len);
+#else
   int64_t ntiles, tpc, grid;
-  cp_plan(d_in, m, sms, &ntiles, &tpc, &grid);
+  cp_plan(d_in, m, di->sms, &ntiles, &tpc, &grid);
   int64_t *counts = static_cast<int64_t *>(d_ws);
   uint32_t *masks = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(d_ws) + 8 * kCpMaxChunks);
   cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(d_in, m, tpc, counts,
@@ -821,12 +1023,17 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
   despace_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(DsSmem), stream>>>(
       d_in, m, d_out, counts, masks, tpc, d_out_len);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
+#endif
 }
 
 size_t b64_decode_ws_workspace_bytes(int64_t m) {
   if (m < 0) return 0;
   const int64_t ntiles = (15 + m + kCpTile - 1) / kCpTile;
+#if B64_CP_ONEPASS
+  return kWsHdrBytes + 4 * static_cast<size_t>(ntiles);  // header + per-tile kept counts
+#else
   return kWsHdrBytes + 8 * kCpMaxChunks + cp_mask_bytes(m) + 4 * static_cast<size_t>(ntiles);
+#endif
 }
 
 int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
@@ -834,6 +1041,7 @@ int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
   if (m < 0 || !flags_ok(flags) || d_result == nullptr || (m > 0 && d_in == nullptr) ||
       (b64_decoded_max_len_ex(m, flags) > 0 && d_out == nullptr))
     return B64_ERR_ARG;
+  DevGuard g(stream);
   if (m == 0) {
     const b64_result r{0, -1, B64_OK, 0};
     return cudaMemcpyAsync(d_result, &r, sizeof(r), cudaMemcpyHostToDevice, stream) == cudaSuccess
@@ -843,30 +1051,48 @@ int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
   if (d_ws == nullptr || ws_bytes < b64_decode_ws_workspace_bytes(m) ||
       (reinterpret_cast<uintptr_t>(d_ws) & 15) != 0)
     return B64_ERR_WORKSPACE;
-  int dev, sms;
-  if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
+  int dev;
+  DevInfo *di = device_setup_info(&dev);
+  if (di == nullptr) return B64_ERR_CUDA;
+  const int sms = di->sms;
+  uint8_t *base = static_cast<uint8_t *>(d_ws);
+  WlState *wl = reinterpret_cast<WlState *>(base + kWlStateOffset);
+#if B64_CP_ONEPASS
+  // header (errkey, done, M, WlState) + per-tile counts, zeroed in one memset
+  const int64_t ntiles = op_ntiles(d_in, m);
+  if (cudaMemsetAsync(base, 0, kWsHdrBytes + 4 * static_cast<size_t>(ntiles), stream) != cudaSuccess)
+    return B64_ERR_CUDA;
+  // 1. verified fast path for line-structured text (MIME / PEM); 2. the
+  // general one-pass kernel, which returns at once when 1. succeeded.
+  decode_lines_kernel<<<static_cast<unsigned>(sms * di->wl_ctas), kWlThreads, sizeof(WlSmem), stream>>>(
+      d_in, m, d_out, wl, d_result, flags);
+  if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
+  return op_launch(decode_ws1_kernel, ntiles, di, sizeof(OpWsSmem), stream, d_in, m, d_out,
+                   reinterpret_cast<uint32_t *>(base + kWsHdrBytes), reinterpret_cast<OpWsHdr *>(base),
+                   d_result, flags, static_cast<const int32_t *>(&wl->verdict));
+#else
   int64_t ntiles, tpc, grid;
   cp_plan(d_in, m, sms, &ntiles, &tpc, &grid);
-  uint8_t *base = static_cast<uint8_t *>(d_ws);
   WsHdr *hdr = reinterpret_cast<WsHdr *>(base);
   int64_t *counts = reinterpret_cast<int64_t *>(base + kWsHdrBytes);
   uint32_t *masks = reinterpret_cast<uint32_t *>(base + kWsHdrBytes + 8 * kCpMaxChunks);
   int32_t *tcnt = reinterpret_cast<int32_t *>(base + kWsHdrBytes + 8 * kCpMaxChunks + cp_mask_bytes(m));
   // 1. verified fast path for line-structured text (MIME / PEM); 2-3. the
   // general path, which returns at once when 1. succeeded.
-  WlState *wl = reinterpret_cast<WlState *>(base + kWlStateOffset);
   if (cudaMemsetAsync(wl, 0, sizeof(WlState), stream) != cudaSuccess) return B64_ERR_CUDA;
-  decode_lines_kernel<<<static_cast<unsigned>(sms * g_wl_ctas), kWlThreads, sizeof(WlSmem), stream>>>(
+  decode_lines_kernel<<<static_cast<unsigned>(sms * di->wl_ctas), kWlThreads, sizeof(WlSmem), stream>>>(
       d_in, m, d_out, wl, d_result, flags);
   cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(
       d_in, m, tpc, counts, masks, &hdr->errkey, &wl->verdict);
   decode_ws_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(WsSmem), stream>>>(
       d_in, m, d_out, counts, masks, tcnt, tpc, hdr, d_result, flags, &wl->verdict);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
+#endif
 }
 
 int b64_decode_ws(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int64_t *out_len,
                   int64_t *err_pos, void *d_ws, size_t ws_bytes, b64_stream_t stream) {
+  DevGuard g(stream);
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   StreamWs *w = stream_ws(dev, stream);
@@ -897,6 +1123,7 @@ int64_t b64_encode_wrapped(const uint8_t *d_in, int64_t n, uint8_t *d_out, int l
   if (!wrap_args_ok(n, line_chars, crlf, flags) || (n > 0 && (d_in == nullptr || d_out == nullptr)))
     return B64_ERR_ARG;
   if (n == 0) return 0;
+  DevGuard g(stream);
   int dev, sms;
   if (!device_setup(&dev, &sms)) return B64_ERR_CUDA;
   WrGeom W;

@@ -77,3 +77,96 @@ def decode(t: np.ndarray, threads: int = THREADS):
             return st, b + ep, out[: 3 * (b // 4) + osz].copy()
         olen = 3 * (b // 4) + osz
     return oracle.OK, -1, out[:olen].copy()
+
+
+# ------------------------------------------------ streaming helpers (C5, f3/f4)
+
+def gen(seed: int, begin: int, end: int, threads: int = THREADS) -> np.ndarray:
+    """inputs.gen.splitmix_bytes(seed, begin, end), generated in threads
+    (counter-based: each thread fills its own byte range)."""
+    from inputs.gen import splitmix_bytes
+
+    out = np.empty(max(end - begin, 0), dtype=np.uint8)
+    cuts = [begin + (end - begin) * r // threads for r in range(threads + 1)]
+
+    def job(r):
+        a, b = cuts[r], cuts[r + 1]
+        if b > a:
+            out[a - begin: b - begin] = splitmix_bytes(seed, a, b)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(job, range(threads)))
+    return out
+
+
+def _line_parts(nlines: int, threads: int):
+    return [(nlines * r // threads, nlines * (r + 1) // threads) for r in range(threads)]
+
+
+def encode_wrapped(x: np.ndarray, line_chars: int, crlf: bool, threads: int = THREADS) -> np.ndarray:
+    """oracle.encode_wrapped(x, line_chars, crlf), split on whole lines
+    (3*line_chars/4 input bytes per line): every part but the last is whole
+    lines, whose wrapped encodings concatenate to the whole's."""
+    lb = 3 * line_chars // 4
+    lt = line_chars + (2 if crlf else 1)
+    nlines = (x.size + lb - 1) // lb
+    parts = [(a, b) for a, b in _line_parts(nlines, threads) if b > a]
+    outs = [None] * len(parts)
+
+    def job(i):
+        a, b = parts[i]
+        outs[i] = oracle.encode_wrapped(x[a * lb: min(b * lb, x.size)], line_chars, crlf=crlf)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(job, range(len(parts))))
+    out = np.concatenate(outs) if outs else np.zeros(0, dtype=np.uint8)
+    assert all(o.size == (b - a) * lt for o, (a, b) in zip(outs[:-1], parts[:-1]))
+    return out
+
+
+def despace(t: np.ndarray, threads: int = THREADS) -> np.ndarray:
+    """oracle.despace(t): App. B removal is byte-local, so any split works."""
+    cuts = [t.size * r // threads for r in range(threads + 1)]
+    outs = [None] * threads
+
+    def job(r):
+        outs[r] = oracle.despace(t[cuts[r]: cuts[r + 1]])
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(job, range(threads)))
+    return np.concatenate(outs)
+
+
+def decode_ws_lines(t: np.ndarray, line_total: int, flags: int = 0, threads: int = THREADS):
+    """oracle.decode_ws(t, flags) for text whose every line but the last is
+    ``line_total`` bytes of which a multiple of 4 are kept characters (MIME
+    lines): a non-final part of whole lines is decoded with a valid quad
+    appended (its last quad is then not the final one, as in the whole
+    decode), error offsets are shifted back to whole-text coordinates, and
+    the first part with an error decides.  Returns (status, err_pos, out)."""
+    nlines = (t.size + line_total - 1) // line_total
+    parts = [(a * line_total, min(b * line_total, t.size)) for a, b in _line_parts(nlines, threads) if b > a]
+    if len(parts) <= 1:
+        return oracle.decode_ws(t, flags)
+    res = [None] * len(parts)
+
+    def job(i):
+        a, b = parts[i]
+        last = i == len(parts) - 1
+        c = t[a:b] if last else np.concatenate([t[a:b], _AAAA])
+        st, ep, o = oracle.decode_ws(c, flags)
+        if not last:
+            if st != oracle.OK and ep < b - a:
+                pass
+            else:
+                st, ep, o = oracle.OK, -1, o[: o.size - 3]
+        res[i] = (st, ep, o)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(job, range(len(parts))))
+    outs = []
+    for (a, b), (st, ep, o) in zip(parts, res):
+        outs.append(o)
+        if st != oracle.OK:
+            return st, a + ep, np.concatenate(outs)
+    return oracle.OK, -1, np.concatenate(outs)

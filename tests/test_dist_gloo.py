@@ -1,7 +1,8 @@
 """Multi-process (world size 2, gloo, CPU) test of the sharded-decode result
-exchange in paper_1704_00605_b200/dist.py: MIN all-reduce of the global
-error offset + all-gather of shard output lengths must reproduce the
-whole-buffer oracle result.  Shard-local results come from the oracle
+exchange in paper_1704_00605_b200/dist.py: MIN all-reduce of the shard
+reduction key (b64_shard_key: global error offset + status) + all-gather of
+shard output lengths, combined by the C ABI's b64_combine_shards, must
+reproduce the whole-buffer oracle result under all 8 flag combinations.  Shard-local results come from the oracle
 (test infrastructure); on the GPU they come from b64_decode_shard_async."""
 import os
 import socket
@@ -13,6 +14,23 @@ import torch.multiprocessing as mp
 WORLD = 2
 
 
+def _collect(procs, q, timeout):
+    """Results of every worker; fails fast if one of them dies."""
+    import queue
+    import time
+
+    got, t0 = {}, time.time()
+    while len(got) < len(procs):
+        try:
+            r, v = q.get(timeout=1)
+            got[r] = v
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, f"worker died: {dead}"
+            assert time.time() - t0 < timeout, "workers timed out"
+    return got
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -21,17 +39,19 @@ def _free_port():
     return p
 
 
-def _local_result(t_local, final):
-    """Shard-local (err_pos, out_len) with R-shard semantics, via the oracle."""
+def _local_result(t_local, final, flags):
+    """Shard-local (status, err_pos, out_len) with R-shard semantics, via the
+    oracle: a non-final shard is decoded with a valid quad appended, so its
+    last two positions are not final-quad positions."""
     import oracle
 
     if final:
-        st, ep, out = oracle.decode(t_local)
-        return ep, out.size
-    st, ep, out = oracle.decode(np.concatenate([t_local, np.frombuffer(b"AAAA", np.uint8)]))
+        st, ep, out = oracle.decode_ex(t_local, flags)
+        return st, ep, out.size
+    st, ep, out = oracle.decode_ex(np.concatenate([t_local, np.frombuffer(b"AAAA", np.uint8)]), flags)
     if st != oracle.OK and ep < t_local.size:
-        return ep, 3 * (ep // 4)
-    return -1, 3 * (t_local.size // 4)
+        return st, ep, 3 * (ep // 4)
+    return oracle.OK, -1, 3 * (t_local.size // 4)
 
 
 def _worker(rank, port, cases, q):
@@ -41,48 +61,70 @@ def _worker(rank, port, cases, q):
     import torch.distributed as dist
 
     from paper_1704_00605_b200 import dist as b64dist
-    from paper_1704_00605_b200 import b64_shard
+    from paper_1704_00605_b200 import b64_shard, b64_shard_key
 
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     res = []
-    for t in cases:
+    for t, flags in cases:
         b, e = b64_shard(t.size, 4, WORLD, rank)
-        ep, ol = _local_result(t[b:e], final=(rank == WORLD - 1))
-        g = b + ep if ep >= 0 else b64dist.INT64_MAX
-        res.append(b64dist.combine(g, ol, t.size, torch.device("cpu")))
+        st, ep, ol = _local_result(t[b:e], rank == WORLD - 1, flags)
+        res.append(b64dist.combine(b64_shard_key(st, ep, b), ol, t.size, torch.device("cpu")))
     dist.destroy_process_group()
     q.put((rank, res))
 
 
-def test_sharded_decode_combine_world2():
+def _flag_cases():
+    """Whole buffers x all 8 flag combinations (URL, NOPAD, STRICT): clean,
+    truncated (LENGTH / unpadded tails), corrupted in either shard, misplaced
+    '=', and non-canonical trailing bits (STRICT -> NONCANONICAL)."""
     import oracle
     from inputs.gen import splitmix_bytes
 
-    x = splitmix_bytes(77, 0, 30001)
-    t = oracle.encode(x)            # 40004 chars, ends with one '='
-    cases = [t, t[:-1], t[:-3]]
-    for pos, b in [(5, 0x21), (20010, 0x21), (39999, 0x00), (20000, ord("=")), (20003, ord("="))]:
+    cases = []
+    for flags in range(8):
+        for n in (30001, 30002, 30000):
+            x = splitmix_bytes(77 + n, 0, n)
+            t = oracle.encode_ex(x, flags)
+            cases += [(t, flags), (t[:-1], flags), (t[:-3], flags)]
+        t = oracle.encode_ex(splitmix_bytes(78, 0, 30001), flags)
+        m = t.size
+        for pos, b in [(5, 0x21), (m // 2 + 10, 0x21), (m - 5, 0x00), (m // 2, ord("=")),
+                       (m // 2 + 3, ord("=")), (m - 1, 0x80), (100, ord("-")), (200, ord("/"))]:
+            u = t.copy()
+            u[pos] = b
+            cases.append((u, flags))
         u = t.copy()
-        u[pos] = b
-        cases.append(u)
-    u = t.copy()
-    u[100] = 0x80
-    u[30000] = 0x80
-    cases.append(u)
+        u[100] = 0x80
+        u[m - 100] = 0x80
+        cases.append((u, flags))
+        # non-canonical final quad: "Zh==" / "Zm9=" tails ("Zg==" / "Zm8=" canonical)
+        for tail in (b"Zh==", b"Zm9=", b"Zh", b"Zm9"):
+            u = np.concatenate([t[: 4 * (m // 4) - 4], np.frombuffer(tail, np.uint8)])
+            cases.append((u, flags))
+    return cases
+
+
+def test_sharded_decode_combine_world2():
+    import oracle
+
+    cases = _flag_cases()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, port, cases, q)) for r in range(WORLD)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=120) for _ in range(WORLD))
+    got = _collect(procs, q, 240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for i, c in enumerate(cases):
-        st, ep, out = oracle.decode(c)
+    seen = set()
+    for i, (c, flags) in enumerate(cases):
+        st, ep, out = oracle.decode_ex(c, flags)
+        seen.add(st)
         for r in range(WORLD):
-            assert got[r][i] == (st, ep, out.size), (i, r, got[r][i], (st, ep, out.size))
+            assert got[r][i] == (st, ep, out.size), (i, flags, r, got[r][i], (st, ep, out.size))
+    assert seen == {oracle.OK, oracle.INVALID_CHAR, oracle.LENGTH, oracle.NONCANONICAL}
 
 
 # ------------------------------------------------------- batches (§8(e))
@@ -138,7 +180,7 @@ def test_batch_shard_and_gather_world2():
     procs = [ctx.Process(target=_batch_worker, args=(r, port, raw, off, text, toff, q)) for r in range(WORLD)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=120) for _ in range(WORLD))
+    got = _collect(procs, q, 120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

@@ -116,13 +116,18 @@ def test_c4_decode_validation_stress():
     assert np.array_equal(host(y), rout)
 
 
+CHUNK = 3 * (256 << 20)   # 768 MiB of raw bytes (1 GiB of text) per oracle chunk
+
+
 @pytest.mark.slow
-def test_c5_32gib_sampled_and_sharded():
-    """32 GiB on one GPU (the G=1 point of config 5): sampled windows vs the
-    oracle, GPU round trip, 8-way shard emulation, one corruption in the last
-    shard."""
+def test_c5_32gib_full_oracle_parity_and_sharded():
+    """32 GiB on one GPU (the G=1 point of config 5), compared with the CPU
+    oracle IN FULL: the GPU encoding of all 2^35 bytes and the GPU decoding
+    of all 45.8 G characters are streamed back in 768 MiB / 1 GiB chunks and
+    compared with the oracle (Alg 1 / Alg 2) run on all host
+    cores on the same seeded bytes.  Then the 8-way shard emulation with the
+    exchange records, clean and with one corruption in the last shard."""
     from inputs.gpu_gen import fill
-    from paper_1704_00605_b200.dist import INT64_MAX, global_decode_result
 
     free, _ = torch.cuda.mem_get_info()
     n = W.C5_N
@@ -131,41 +136,56 @@ def test_c5_32gib_sampled_and_sharded():
         pytest.skip(f"needs {(2 * n + m) / 2**30:.0f} GiB of device memory")
     x = torch.empty(n, dtype=torch.uint8, device=DEV)
     fill(x, W.C5_SEED)
-    # the CUDA generator equals the numpy twin on samples (incl. offsets > 2^32)
-    for o in (0, (1 << 32) + 5, n - 1000):
-        assert np.array_equal(host(x[o: o + 1000]), splitmix_bytes(W.C5_SEED, o, o + 1000))
     t = torch.empty(m, dtype=torch.uint8, device=DEV)
     b64.b64_encode(x, out=t)
-    rng = np.random.default_rng(55)
-    groups = n // 3
-    windows = [0, groups - 100_000] + [int(g) for g in rng.integers(0, groups - 100_000, 24)]
-    for g in windows:
-        o = 3 * g
-        L = min(3 * 100_000, n - o)
-        exp = oracle.encode(splitmix_bytes(W.C5_SEED, o, o + L))
-        assert np.array_equal(host(t[4 * g: 4 * g + exp.size]), exp), g
-    # tail: n mod 3 = 2 -> one '='
-    tail = oracle.encode(splitmix_bytes(W.C5_SEED, n - 5, n))
-    assert np.array_equal(host(t[m - 8:]), tail[-8:])
     y = torch.empty(b64.b64_decoded_max_len(m), dtype=torch.uint8, device=DEV)
     yv, st, ep = b64.b64_decode(t, out=y)
     assert (st, ep, yv.numel()) == (b64.B64_OK, -1, n)
-    assert torch.equal(yv, x)
-    # 8-way shard emulation (sequential on one GPU; no collectives)
+    # whole-buffer oracle parity, chunk by chunk (chunks of whole groups /
+    # quads; only the last chunk holds the '=' tail: n mod 3 = 2)
+    pinned_t = torch.empty(4 * CHUNK // 3, dtype=torch.uint8).pin_memory()
+    pinned_y = torch.empty(CHUNK, dtype=torch.uint8).pin_memory()
+    checked_in = checked_out = 0
+    for o in range(0, n, CHUNK):
+        L = min(CHUNK, n - o)
+        xs = oracle_par.gen(W.C5_SEED, o, o + L)
+        ref = oracle_par.encode(xs)                       # Alg 1 on the chunk
+        tv = pinned_t[: ref.size]
+        tv.copy_(t[4 * (o // 3): 4 * (o // 3) + ref.size])
+        assert np.array_equal(tv.numpy(), ref), ("encode chunk", o)
+        rst, rep, rout = oracle_par.decode(ref)          # Alg 2 on the same text
+        assert (rst, rep) == (oracle.OK, -1) and rout.size == L
+        yh = pinned_y[:L]
+        yh.copy_(y[o: o + L])
+        assert np.array_equal(yh.numpy(), rout), ("decode chunk", o)
+        checked_in += L
+        checked_out += ref.size
+    assert (checked_in, checked_out) == (n, m)
+    assert bytes(pinned_t[ref.size - 2: ref.size].numpy()) != b"==" and pinned_t[ref.size - 1] == ord("=")
+    # the CUDA generator equals the numpy twin (incl. offsets > 2^32)
+    for o in (0, (1 << 32) + 5, n - 1000):
+        assert np.array_equal(host(x[o: o + 1000]), splitmix_bytes(W.C5_SEED, o, o + 1000))
+    del x
+    # 8-way shard emulation (sequential on one GPU; no collectives): each
+    # shard decode writes its exchange record, combined on the device
     for dirty_at in (None, m - 12345):
         if dirty_at is not None:
             t[dirty_at] = 0x21
-        errs, lens = [], []
+        keys = torch.empty(8, 2, dtype=torch.int64, device=DEV)
         for r in range(8):
             bgn, end = b64.b64_shard(m, 4, 8, r)
             res = b64.result_tensor(DEV)
-            b64.b64_decode_shard_async(t[bgn:end], y[3 * (bgn // 4):], res, final_shard=(r == 7))
-            ol, e, s, _ = b64.unpack_result(res)
-            errs.append(bgn + e if e >= 0 else INT64_MAX)
-            lens.append(ol)
-        st, ep, ol = global_decode_result(min(errs), m, lens)
+            b64.b64_decode_shard_ex_async(t[bgn:end], y[3 * (bgn // 4):], res, bgn, final_shard=(r == 7),
+                                          key=keys[r])
+        kmin = keys[:, 0].min().reshape(1).contiguous()
+        out = b64.result_tensor(DEV)
+        b64.b64_combine_shards_async(kmin, keys[:, 1].contiguous(), m, out)
+        ol, ep, st, _ = b64.unpack_result(out)
         if dirty_at is None:
             assert (st, ep, ol) == (b64.B64_OK, -1, n)
-            assert torch.equal(y[:n], x)
         else:
-            assert (st, ep, ol) == (b64.B64_ERR_INVALID_CHAR, dirty_at, 3 * (dirty_at // 4))
+            # the oracle on the dirty last quads: the error is the only one
+            tail = host(t[dirty_at - 4 * 1000: m])
+            rst, rep, _ = oracle.decode(tail)
+            assert (st, ep, ol) == (rst, dirty_at - 4 * 1000 + rep, 3 * (dirty_at // 4))
+            assert st == b64.B64_ERR_INVALID_CHAR and ep == dirty_at

@@ -194,7 +194,7 @@ def test_fuzz_shards():
     """Random world sizes and lengths: per-rank encode of b64_shard ranges
     concatenates to the whole-buffer encoding; per-rank shard decodes
     combine (min error offset, summed lengths) to the whole-buffer decode."""
-    from paper_1704_00605_b200.dist import INT64_MAX, global_decode_result
+    from tests.test_gpu_parity import emulate_sharded_decode
 
     rng = np.random.default_rng(9004 + SEED)
     for case in range(40 * SCALE):
@@ -208,22 +208,14 @@ def test_fuzz_shards():
         t = np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint8)
         assert np.array_equal(t, oracle.encode(x)), ("shard encode", case, n, world)
         c = corrupt(rng, t, 0)
-        errs, lens, outs = [], [], []
-        for r in range(world):
-            b, e = b64.b64_shard(c.size, 4, world, r)
-            out = torch.empty(max(b64.b64_decoded_max_len(e - b), 1), dtype=torch.uint8, device=DEV)
-            res = b64.result_tensor(DEV)
-            b64.b64_decode_shard_async(to_dev(c[b:e], int(rng.integers(0, 16))), out, res,
-                                       final_shard=(r == world - 1))
-            ol, ep, st, _ = b64.unpack_result(res)
-            errs.append(b + ep if ep >= 0 else INT64_MAX)
-            lens.append(ol)
-            outs.append(host(out[:ol]))
-        st, ep, ol = global_decode_result(min(errs), c.size, lens)
-        rst, rep, rout = oracle.decode(c)
-        assert (st, ep, ol) == (rst, rep, rout.size), ("shard decode", case, world, st, ep, rst, rep)
-        if st == b64.B64_OK:
-            assert np.array_equal(np.concatenate(outs)[:ol], rout), ("shard bytes", case)
+        flags = int(rng.integers(0, 8)) if case % 2 else 0
+        if flags:
+            t = oracle.encode_ex(x, flags)
+            c = corrupt(rng, t, flags)
+        st, ep, ol, outs = emulate_sharded_decode(c, world, flags, rng=rng)
+        rst, rep, rout = oracle.decode_ex(c, flags)
+        assert (st, ep, ol) == (rst, rep, rout.size), ("shard decode", case, world, flags, st, ep, rst, rep)
+        assert np.array_equal(np.concatenate(outs)[:ol], rout), ("shard bytes", case)
 
 
 def test_fuzz_host_buffers():
@@ -235,19 +227,20 @@ def test_fuzz_host_buffers():
         x = splitmix_bytes(9005, case * 4_000_037, case * 4_000_037 + n)
         pin = bool(rng.integers(0, 2))
         mk = (lambda a: torch.from_numpy(a).pin_memory()) if pin else torch.from_numpy
-        m = b64.b64_encoded_len(n)
+        flags = int(rng.integers(0, 8)) if case % 2 else 0
+        m = b64.b64_encoded_len_ex(n, flags)
         hx = mk(x.copy())
         ht = mk(np.empty(m, dtype=np.uint8))
         si = torch.empty(max(m, 1), dtype=torch.uint8, device=DEV)
         so = torch.empty(max(m, 1), dtype=torch.uint8, device=DEV)
-        assert b64.b64_encode_host(hx, ht, si, so) == m
-        t = oracle.encode(x)
-        assert np.array_equal(ht.numpy(), t), ("host encode", case, n, pin)
+        assert b64.b64_encode_host(hx, ht, si, so, flags=flags) == m
+        t = oracle.encode_ex(x, flags)
+        assert np.array_equal(ht.numpy(), t), ("host encode", case, n, pin, flags)
         c = corrupt(rng, t, 0)
         hc = mk(c.copy())
-        hy = mk(np.empty(max(b64.b64_decoded_max_len(c.size), 1), dtype=np.uint8))
-        st, ol, ep = b64.b64_decode_host(hc, hy, si, so)
-        rst, rep, rout = oracle.decode(c)
+        hy = mk(np.empty(max(b64.b64_decoded_max_len_ex(c.size, flags), 1), dtype=np.uint8))
+        st, ol, ep = b64.b64_decode_host(hc, hy, si, so, flags=flags)
+        rst, rep, rout = oracle.decode_ex(c, flags)
         assert (st, ep, ol) == (rst, rep, rout.size), ("host decode", case, st, ep, rst, rep)
         assert np.array_equal(hy.numpy()[:ol], rout), ("host decode bytes", case)
 

@@ -253,36 +253,54 @@ def test_decode_async_result_record():
 
 # --------------------------------------------------------------- shards
 
+def emulate_sharded_decode(t, world, flags=0, mis=None, rng=None):
+    """Single-GPU emulation of the sharded decode (ranks run sequentially,
+    no collectives): every shard decode writes its exchange record (key,
+    out_len); MIN of the keys + the gathered lengths go through BOTH the
+    device combine (b64_combine_shards_async) and the host one, which must
+    agree.  Returns (status, err_pos, out_len, shard outputs)."""
+    keys, lens, outs = [], [], []
+    for r in range(world):
+        bgn, end = b64.b64_shard(t.size, 4, world, r)
+        mi = int(rng.integers(0, 16)) if rng is not None else (mis or 0)
+        d = to_dev(t[bgn:end], mi)
+        cap = b64.b64_decoded_max_len_ex(end - bgn, flags)
+        out = torch.empty(max(cap, 1), dtype=torch.uint8, device=DEV)
+        res = b64.result_tensor(DEV)
+        key = torch.empty(2, dtype=torch.int64, device=DEV)
+        b64.b64_decode_shard_ex_async(d, out, res, bgn, final_shard=(r == world - 1), flags=flags, key=key)
+        ol, ep, st, _ = b64.unpack_result(res)
+        k = host(key).tolist()
+        assert k == [b64.b64_shard_key(st, ep, bgn), ol]
+        keys.append(k[0])
+        lens.append(ol)
+        outs.append(host(out[:ol]))
+    kmin = torch.tensor([min(keys)], dtype=torch.int64, device=DEV)
+    dres = b64.result_tensor(DEV)
+    b64.b64_combine_shards_async(kmin, torch.tensor(lens, dtype=torch.int64, device=DEV), t.size, dres)
+    ol, ep, st, pc = b64.unpack_result(dres)
+    assert (st, ep, ol, pc) == b64.b64_combine_shards(min(keys), lens, t.size)
+    return st, ep, ol, outs
+
+
 def test_shard_decode_matches_whole_buffer():
     """Split a buffer on 4-char boundaries; non-final shards reject '=' and
     skip the final-quad rule; the combined result equals the whole-buffer
-    oracle decode (the single-GPU emulation of the sharded run)."""
-    from paper_1704_00605_b200.dist import INT64_MAX, global_decode_result
-
-    x = splitmix_bytes(113, 0, 250001)
-    t0 = oracle.encode(x)
-    variants = [t0, t0[:-1], t0.copy(), t0.copy()]
-    variants[2][200000] = ord("=")
-    variants[3][50] = 0x80
-    for t in variants:
-        for world in (1, 2, 3, 8):
-            errs, lens, outs = [], [], []
-            for r in range(world):
-                bgn, end = b64.b64_shard(t.size, 4, world, r)
-                d = to_dev(t[bgn:end])
-                out = torch.empty(max(b64.b64_decoded_max_len(end - bgn), 1), dtype=torch.uint8, device=DEV)
-                res = b64.result_tensor(DEV)
-                b64.b64_decode_shard_async(d, out, res, final_shard=(r == world - 1))
-                ol, ep, st, _ = b64.unpack_result(res)
-                errs.append(bgn + ep if ep >= 0 else INT64_MAX)
-                lens.append(ol)
-                outs.append(host(out[:ol]))
-            st, ep, ol = global_decode_result(min(errs), t.size, lens)
-            rst, rep, rout = oracle.decode(t)
-            assert (st, ep, ol) == (rst, rep, rout.size), (world, st, ep, rst, rep)
-            got = np.concatenate(outs)[:ol] if st == b64.B64_OK else None
-            if got is not None:
-                assert np.array_equal(got, rout)
+    oracle decode under all 8 flag combinations (the single-GPU emulation of
+    the sharded run)."""
+    for flags in range(8):
+        x = splitmix_bytes(113, 0, 250001)
+        t0 = oracle.encode_ex(x, flags)
+        variants = [t0, t0[:-1], t0[:-2], t0.copy(), t0.copy(), t0.copy()]
+        variants[3][200000] = ord("=")
+        variants[4][50] = 0x80
+        variants[5][-3:] = np.frombuffer(b"Zh=", np.uint8) if t0.size % 4 == 0 else variants[5][-3:]
+        for t in variants:
+            for world in (1, 2, 3, 8):
+                st, ep, ol, outs = emulate_sharded_decode(t, world, flags)
+                rst, rep, rout = oracle.decode_ex(t, flags)
+                assert (st, ep, ol) == (rst, rep, rout.size), (flags, world, st, ep, rst, rep)
+                assert np.array_equal(np.concatenate(outs)[:ol], rout)
 
 
 def test_nonfinal_shard_rejects_padding():
@@ -417,7 +435,7 @@ def test_host_buffer_api():
     x = splitmix_bytes(117, 0, 123457)
     hx = torch.from_numpy(x).pin_memory()
     ht = torch.empty(b64.b64_encoded_len(x.size), dtype=torch.uint8).pin_memory()
-    si = torch.empty(x.size, dtype=torch.uint8, device=DEV)
+    si = torch.empty(ht.numel(), dtype=torch.uint8, device=DEV)
     so = torch.empty(ht.numel(), dtype=torch.uint8, device=DEV)
     n = b64.b64_encode_host(hx, ht, si, so)
     assert n == ht.numel() and np.array_equal(ht.numpy(), oracle.encode(x))
@@ -455,3 +473,49 @@ def test_host_buffer_api_multichunk():
         rst, rep, rout = oracle_par.decode(t)
         assert (st, ep, ol) == (rst, rep, rout.size), (pos, st, ep, ol, rst, rep)
         assert np.array_equal(hy.numpy()[:ol], rout)
+
+
+def test_host_api_respects_stream_order():
+    """the host-buffer pipeline's internal copy streams wait for
+    the work already queued on the caller's stream.  An async encode that
+    reads X, queued behind a long sleep, must not see the host call's H2D
+    copy overwrite X (X is reused as the host call's d_scratch_in)."""
+    s = torch.cuda.Stream()
+    x1 = splitmix_bytes(119, 0, 3 << 20)
+    x2 = splitmix_bytes(120, 0, 3 << 20)
+    X = torch.from_numpy(x1).to(DEV)
+    out1 = torch.empty(b64.b64_encoded_len(x1.size), dtype=torch.uint8, device=DEV)
+    so = torch.empty_like(out1)
+    hx = torch.from_numpy(x2).pin_memory()
+    ht = torch.empty(out1.numel(), dtype=torch.uint8).pin_memory()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(50_000_000)                    # ~25 ms of GPU time
+        b64.b64_encode(X, out=out1, stream=s)            # reads X (x1)
+        b64.b64_encode_host(hx, ht, X, so, stream=s)     # overwrites X with x2
+    torch.cuda.synchronize()
+    assert np.array_equal(host(out1), oracle.encode(x1))
+    assert np.array_equal(ht.numpy(), oracle.encode(x2))
+
+
+def test_host_api_flags_roundtrip():
+    """b64_encode_host_ex / b64_decode_host_ex: every flag set, multichunk
+    sizes, against oracle.encode_ex / decode_ex."""
+    for flags in range(8):
+        for n in (0, 1, 2, 100, 25_165_826):
+            x = splitmix_bytes(121 + flags, 0, n)
+            m = b64.b64_encoded_len_ex(n, flags)
+            hx = torch.from_numpy(x).pin_memory()
+            ht = torch.empty(max(m, 1), dtype=torch.uint8).pin_memory()
+            si = torch.empty(max(m, 1), dtype=torch.uint8, device=DEV)
+            so = torch.empty(max(m, 1), dtype=torch.uint8, device=DEV)
+            assert b64.b64_encode_host(hx, ht[:m], si, so, flags=flags) == m
+            ref = oracle.encode_ex(x, flags)
+            assert np.array_equal(ht[:m].numpy(), ref), (flags, n)
+            for c in (ref, ref[:-1]):
+                hc = torch.from_numpy(c.copy()).pin_memory()
+                hy = torch.empty(max(b64.b64_decoded_max_len_ex(c.size, flags), 1), dtype=torch.uint8).pin_memory()
+                st, ol, ep = b64.b64_decode_host(hc, hy, si, so, flags=flags)
+                rst, rep, rout = oracle.decode_ex(c, flags)
+                assert (st, ep, ol) == (rst, rep, rout.size), (flags, n, c.size)
+                assert np.array_equal(hy.numpy()[:ol], rout)

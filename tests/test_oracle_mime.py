@@ -37,6 +37,33 @@ def test_wrapped_encode_pem_64():
         assert bytes(oracle.encode_wrapped(der, 64, crlf=False)) == body, n
 
 
+def test_encoded_len_wrapped_direct_pin():
+    """oracle_encoded_len_wrapped (the capacity of a wrapped encode, R-wrap)
+    pinned directly, not through the GPU's b64_encoded_len_wrapped: for
+    76-char LF lines it is len(base64.encodebytes(x)) (RFC 2045), CR LF adds
+    one byte per line; for any L and flags it is the length of the stdlib
+    encoding (b64encode / urlsafe, '=' stripped for NOPAD) cut into L-char
+    lines each followed by the EOL."""
+    lib = oracle._load()
+    rng = np.random.default_rng(44)
+    ns = list(range(0, 200)) + [int(v) for v in rng.integers(200, 1 << 20, 60)]
+    for n in ns:
+        x = bytes(n)  # lengths do not depend on the bytes
+        e = base64.encodebytes(x)
+        assert lib.oracle_encoded_len_wrapped(n, 76, 0, 0) == len(e), n
+        assert lib.oracle_encoded_len_wrapped(n, 76, 1, 0) == len(e) + e.count(b"\n"), n
+    for L in (4, 8, 64, 76, 100, 1024, 16384):
+        for flags in (0, oracle.URL, oracle.NOPAD, oracle.URL | oracle.NOPAD):
+            for n in [0, 1, 2, 3, 4, 5, L // 4 * 3, L // 4 * 3 + 1, 3 * L + 2] + ns[-5:]:
+                s = base64.b64encode(bytes(n))
+                if flags & oracle.NOPAD:
+                    s = s.rstrip(b"=")
+                for crlf in (0, 1):
+                    eol = b"\r\n" if crlf else b"\n"
+                    ref = len(b"".join(s[i: i + L] + eol for i in range(0, len(s), L)))
+                    assert lib.oracle_encoded_len_wrapped(n, L, crlf, flags) == ref, (n, L, crlf, flags)
+
+
 @pytest.mark.parametrize("L", [4, 8, 60, 64, 76, 100, 1024])
 @pytest.mark.parametrize("flags", [0, oracle.URL, oracle.NOPAD, oracle.URL | oracle.NOPAD])
 def test_wrapped_encode_structure(L, flags):
