@@ -204,7 +204,7 @@ struct alignas(128) CpSmem {
   uint32_t msk[kCpStages][kCpThreads];     // the tiles' keep masks (cp_mask_kernel)
   uint64_t full[kCpStages];
   int32_t wcnt[2][kCpWarps];  // by tile parity: back-to-back compactions need no extra barrier
-  uint32_t ktab[16];  // per 4-bit keep mask: PRMT selector (bits 0..15) | (2^c - 1) << 16
+  uint32_t ktab[16];  // per 4-bit keep mask: PRMT selector (bits 0..15) | (2^c - 1) << 16 | c << 20
 };
 
 // Fill CpSmem::ktab (threads 0..15); needs a barrier before use.
@@ -217,7 +217,7 @@ __device__ __forceinline__ void init_ktab(uint32_t *ktab) {
         sel = (sel & ~(0xFu << (4 * c))) | (static_cast<uint32_t>(j) << (4 * c));
         ++c;
       }
-    ktab[k] = sel | (((1u << c) - 1u) << 16);
+    ktab[k] = sel | (((1u << c) - 1u) << 16) | (c << 20);
   }
 }
 
@@ -321,15 +321,17 @@ __device__ __forceinline__ int compact_tile(const uint8_t *win, const uint32_t *
 // CTA-wide copy of n bytes from smem src to global dst, where src and dst
 // are congruent mod 16: aligned LDS.128 -> STG.128 for the interior, byte
 // stores for the (< 16 byte) edges.
-__device__ __forceinline__ void cta_copy_out_congruent(uint8_t *dst, const uint8_t *src, int n) {
+__device__ __forceinline__ void cta_copy_out_congruent(uint8_t *dst, const uint8_t *src, int n,
+                                                       int nthreads = -1) {
   const int tid = threadIdx.x;
+  const int nt = nthreads > 0 ? nthreads : static_cast<int>(blockDim.x);
   const uintptr_t g = reinterpret_cast<uintptr_t>(dst);
   const uintptr_t a0 = (g + 15) & ~static_cast<uintptr_t>(15);
   const uintptr_t a1 = (g + static_cast<uintptr_t>(n)) & ~static_cast<uintptr_t>(15);
   if (a1 > a0) {
     const int head = static_cast<int>(a0 - g);
     const int ng = static_cast<int>((a1 - a0) >> 4);
-    for (int q = tid; q < ng; q += blockDim.x)
+    for (int q = tid; q < ng; q += nt)
       *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(a0) + 16 * q) =
           ptx::lds128(src + head + 16 * q);  // congruent: 16-byte aligned
     const int tail0 = static_cast<int>(a1 - g);

@@ -34,6 +34,12 @@
 #define B64_BATCH_PREFETCH 0
 #endif
 
+// f3 / f4 general path: the single-read kernels of b64_onepass.cuh instead
+// of the two-pass mask + compaction kernels (slower).
+#ifndef B64_CP_ONEPASS
+#define B64_CP_ONEPASS 0
+#endif
+
 // (defined or not; no default)
 //   B64_BATCH_TRACE      per-warp %globaltimer stamps + b64_debug_trace()
 //                        (tools/batch_trace.py); the export is not in the

@@ -29,13 +29,13 @@
 #include "b64_ws.cuh"
 #include "b64_wrap.cuh"
 #include "b64_wslines.cuh"
-#include "b64_onepass.cuh"
 
-// f3 / f4 general path: single-read kernels (b64_onepass.cuh) or the
-// two-pass mask + compaction kernels (b64_compact.cuh, b64_ws.cuh; kept for
-// A/B measurement only).
-#ifndef B64_CP_ONEPASS
-#define B64_CP_ONEPASS 0
+// f3 / f4 general path: the two-pass mask + compaction kernels
+// (b64_compact.cuh, b64_ws.cuh).  B64_CP_ONEPASS=1 (measurement only, see
+// b64_knobs.cuh) builds the single-read kernels of b64_onepass.cuh instead;
+// measured slower on every geometry tried.
+#if B64_CP_ONEPASS
+#include "b64_onepass.cuh"
 #endif
 
 namespace b64 {
@@ -476,6 +476,7 @@ DevInfo *device_setup_info(int *dev_out) {
     if (set_smem(encode_wrap_kernel<2, false>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
     if (set_smem(encode_wrap_kernel<1, false>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
+#if B64_CP_ONEPASS
     if (set_smem(despace1_kernel, sizeof(OpDsSmem)) != cudaSuccess) return nullptr;
     if (set_smem(decode_ws1_kernel, sizeof(OpWsSmem)) != cudaSuccess) return nullptr;
     int o1 = 0, o2 = 0;
@@ -486,6 +487,7 @@ DevInfo *device_setup_info(int *dev_out) {
       return nullptr;
     di.op_ctas = o1 < o2 ? o1 : o2;
     if (di.op_ctas < 1) return nullptr;
+#endif
     di.attrs_set = true;
   }
   *dev_out = dev;
@@ -609,6 +611,7 @@ size_t ws_layout(int64_t k, size_t *off_units, size_t *off_done) {
   return (o + 255) & ~static_cast<size_t>(255);
 }
 
+#if B64_CP_ONEPASS
 int64_t op_ntiles(const void *d_in, int64_t m) {
   const int64_t imis = static_cast<int64_t>(reinterpret_cast<uintptr_t>(d_in) & 15);
   return (imis + m + kCpTile - 1) / kCpTile;
@@ -627,6 +630,7 @@ int op_launch(void (*k)(A...), int64_t ntiles, const DevInfo *di, size_t smem,
              ? B64_OK
              : B64_ERR_CUDA;
 }
+#endif
 
 }  // namespace
 

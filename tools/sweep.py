@@ -180,6 +180,15 @@ VARIANTS = {
     "wl_nodirect": {"B64_WL_DIRECT": 0},
     "wl_direct": {"B64_WL_DIRECT": 1},
     "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
+    # one-pass compaction (f3 / f4 general path)
+    "cp_onepass": {"B64_CP_ONEPASS": 1},
+    "op_s7_l3": {"B64_CP_ONEPASS": 1, "B64_OP_SLOTS": 7, "B64_OP_LAG": 3},
+    "op_s8_l5": {"B64_CP_ONEPASS": 1, "B64_OP_SLOTS": 8, "B64_OP_LAG": 5},
+    "op_s6_l2": {"B64_CP_ONEPASS": 1, "B64_OP_SLOTS": 6, "B64_OP_LAG": 2},
+    "op_c2_s5_l2": {"B64_CP_ONEPASS": 1, "B64_OP_CTAS": 2, "B64_OP_SLOTS": 5, "B64_OP_LAG": 2,
+                    "B64_OP_SCANK": 16},
+    "op_c2_s5_l3": {"B64_CP_ONEPASS": 1, "B64_OP_CTAS": 2, "B64_OP_SLOTS": 5, "B64_OP_LAG": 3,
+                    "B64_OP_SCANK": 16},
 }
 
 
