@@ -1,14 +1,25 @@
 #!/bin/bash
 # Round-end evidence on the GPU box: plain runs first (must exit 0), then
-#  * ncu --set full of encode_kernel / decode_kernel on C3 (one launch each)
-#  * ncu --set full of the batched kernels on C2
-#  * ncu --set full of the f3/f4 kernels (despace, mime workloads)
 #  * DRAM bytes of the C5 launches (single-pass metrics, no replay of 80 GB)
-#  * the launch list (gpu__time_duration) of the default bench command
+#    -> profiles/ncu_traffic.json stamped with the source sha (tools/traffic_json.py),
+#    BEFORE the default bench, so its roofline.traffic comes from this build
+#  * the default bench line and the launch list (gpu__time_duration) of the same command
+#  * ncu --set full of encode_kernel / decode_kernel on C3 (one launch each)
+#  * ncu --set full of the batched kernels on C2, the f3/f4 kernels (despace, mime workloads)
 set -u
-T=${1:-r01}
+T=${1:-r02}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { echo build failed; exit 1; }
+B5="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu"
+$B5 > gpurun_out/${T}_c5plain.json 2>&1 && \
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:"(en|de)code_kernel" -s 6 -c 2 --csv --log-file gpurun_out/${T}_c5_traffic.csv $B5 > /dev/null 2>&1
+python tools/traffic_json.py gpurun_out/${T}_c5_traffic.csv $T > gpurun_out/${T}_traffic.log 2>&1; echo "traffic rc=$?"
+cp profiles/ncu_traffic.json gpurun_out/${T}_ncu_traffic.json
+D="python bench.py"
+$D > gpurun_out/${T}_bench_plain.json 2> gpurun_out/${T}_bench_plain.err && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/${T}_launches.csv $D > gpurun_out/${T}_ncu_launch.log 2>&1
 NCU="ncu --set full --clock-control none --import-source on"
 B3="python bench.py --workload c3 --steps 2 --warmup 3 --no-e2e --no-cpu"
 $B3 > gpurun_out/${T}_c3plain.json 2>&1 || { echo "c3 plain failed"; exit 1; }
@@ -26,14 +37,6 @@ $NCU -k regex:"encode_wrap|decode_lines" -s 6 -c 2 -o gpurun_out/${T}_mime -f $B
 BI="python bench.py --workload mime_irregular --steps 1 --warmup 3"
 $BI > gpurun_out/${T}_mimeirrplain.json 2>&1 && \
 $NCU -k regex:"cp_mask|decode_ws" -s 6 -c 2 -o gpurun_out/${T}_mimeirr -f $BI > gpurun_out/${T}_ncu_mimeirr.log 2>&1
-B5="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu"
-$B5 > gpurun_out/${T}_c5plain.json 2>&1 && \
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    -k regex:"(en|de)code_kernel" -s 6 -c 2 --csv --log-file gpurun_out/${T}_c5_traffic.csv $B5 > /dev/null 2>&1
-D="python bench.py"
-$D > gpurun_out/${T}_bench_plain.json 2> gpurun_out/${T}_bench_plain.err && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file gpurun_out/${T}_launches.csv $D > gpurun_out/${T}_ncu_launch.log 2>&1
 for w in c1 c2 c4 despace mime mime_irregular sweep; do
   python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/${T}_bench_$w.json 2> gpurun_out/${T}_bench_$w.err
 done
