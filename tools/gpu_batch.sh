@@ -9,3 +9,6 @@ for r in 1 2 3; do
   timeout 300 python bench.py --workload c2 --steps 20 --warmup 3 > gpurun_out/${T}_bench_c2_$r.json 2> gpurun_out/${T}_bench_c2_$r.err
   python -c "import json;d=json.load(open('gpurun_out/${T}_bench_c2_$r.json'));print('c2', d['detail']['encode_ms'], d['detail']['decode_ms'], d['detail']['graph_replay_ms'], d['roofline']['frac'])"
 done
+if [ -n "${VARIANTS:-}" ]; then
+  python tools/sweep.py run --workload c2 --steps 20 --reps ${REPS:-3} $VARIANTS > gpurun_out/${T}_sweep.log 2>&1; cut -c1-230 gpurun_out/${T}_sweep.log
+fi
