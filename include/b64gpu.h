@@ -34,7 +34,8 @@
  *    stream): two decodes that may run concurrently (e.g. CUDA graphs
  *    captured on the same stream and replayed at once, or replayed on
  *    another stream while direct decodes run on the capture stream) must
- *    have been enqueued on distinct streams.
+ *    have been enqueued on distinct streams -- or use
+ *    b64_decode_scratch_async with distinct caller-owned scratch records.
  */
 #ifndef B64GPU_H
 #define B64GPU_H
@@ -137,6 +138,16 @@ int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int
                   int64_t *err_pos, b64_stream_t stream);
 int b64_decode_ex_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
                         b64_result *d_result, b64_stream_t stream);
+
+/* b64_decode_ex_async with caller-owned scratch instead of the library's
+ * per-(device, stream) record: d_scratch is B64_DECODE_SCRATCH_BYTES of
+ * device memory, 8-byte aligned, ZERO before its first use (cudaMemset);
+ * every call leaves it zero again when its kernel completes.  Decodes that
+ * may run concurrently (e.g. CUDA graphs replayed at the same time) must
+ * use distinct scratch records.  Returns B64_OK if enqueued. */
+#define B64_DECODE_SCRATCH_BYTES 16
+int b64_decode_scratch_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
+                             b64_result *d_result, void *d_scratch, b64_stream_t stream);
 
 /* Decode of one shard of a larger buffer split on 4-character boundaries
  * (multi-GPU sharder).  final_shard != 0: identical to

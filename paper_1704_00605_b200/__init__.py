@@ -51,6 +51,8 @@ from ._lib import (  # noqa: F401
     b64_combine_shards_async,
     b64_decode_shard_ex_async,
     INT64_MAX,
+    b64_decode_scratch_async,
+    scratch_tensor,
     b64_status_str,
     lib_path,
     load_library,

@@ -37,8 +37,9 @@ EXPORTS = (
     "b64_decode_ws_workspace_bytes", "b64_decode_ws", "b64_decode_ws_async",
     "b64_encoded_len_wrapped", "b64_encode_wrapped",
     "b64_decode_shard_ex_async", "b64_shard_key", "b64_combine_shards", "b64_combine_shards_async",
-    "b64_encode_host_ex", "b64_decode_host_ex",
+    "b64_encode_host_ex", "b64_decode_host_ex", "b64_decode_scratch_async",
 )
+B64_DECODE_SCRATCH_BYTES = 16
 INT64_MAX = (1 << 63) - 1
 
 _lib = None
@@ -105,6 +106,7 @@ def load_library():
         "b64_combine_shards": (i32, [i64, vp, i32, i64, ctypes.POINTER(_Result)]),
         "b64_combine_shards_async": (i32, [vp, vp, i32, i64, vp, vp]),
         "b64_encode_host_ex": (i64, [vp, i64, vp, i32, vp, vp, vp]),
+        "b64_decode_scratch_async": (i32, [vp, i64, vp, i32, vp, vp, vp]),
         "b64_decode_host_ex": (i32, [vp, i64, vp, i32, p64, p64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -263,6 +265,29 @@ def b64_decode_ex_async(inp, out, result, flags: int, stream=None):
                                             result.data_ptr(), _stream(stream, inp.device))
     if rc < 0:
         raise B64Error(rc, "b64_decode_ex_async")
+
+
+def scratch_tensor(device):
+    """A zeroed caller-owned decode scratch record (B64_DECODE_SCRATCH_BYTES)."""
+    import torch
+
+    return torch.zeros(B64_DECODE_SCRATCH_BYTES // 8, dtype=torch.int64, device=device)
+
+
+def b64_decode_scratch_async(inp, out, result, scratch, flags: int = 0, stream=None):
+    """Asynchronous decode with a caller-owned scratch record (scratch_tensor):
+    safe for concurrently replayed CUDA graphs that use distinct records."""
+    import torch
+
+    _check_dec_args(inp, out, result, flags)
+    if not (isinstance(scratch, torch.Tensor) and scratch.is_cuda and scratch.is_contiguous() and
+            scratch.numel() * scratch.element_size() >= B64_DECODE_SCRATCH_BYTES):
+        raise TypeError("scratch must be a contiguous CUDA tensor of >= 16 bytes (scratch_tensor)")
+    rc = load_library().b64_decode_scratch_async(_ptr(inp), inp.numel(), _ptr(out), flags,
+                                                 result.data_ptr(), scratch.data_ptr(),
+                                                 _stream(stream, inp.device))
+    if rc < 0:
+        raise B64Error(rc, "b64_decode_scratch_async")
 
 
 def b64_decode_shard_async(inp, out, result, final_shard=True, stream=None):

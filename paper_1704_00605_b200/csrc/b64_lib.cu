@@ -67,11 +67,12 @@ constexpr int kSmallPasses = B64_SMALL_PASSES;
 template <int P> using EncSmemP = Smem<EncG<P>::kIn, EncG<P>::kOut>;
 template <int P> using DecSmemP = Smem<DecG<P>::kIn, DecG<P>::kOut>;
 
-struct DecWs {                 // per-(device, stream) decode scratch (self-resetting)
-  unsigned long long errkey;   // min error offset, ~0 = none
+struct DecWs {                 // decode scratch: zero before the first use, left zero by every call
+  unsigned long long errinv;   // ~(min error offset); 0 = none (atomicMax of the complement)
   unsigned int done;           // CTAs finished
   unsigned int pad;
 };
+static_assert(sizeof(DecWs) == B64_DECODE_SCRATCH_BYTES, "DecWs is the caller-visible scratch record");
 
 // ------------------------------------------- multi-GPU result exchange ---
 // the shards of one buffer are decoded independently; the
@@ -323,9 +324,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       if (werr != 0xFFFFFFFFu) {
         // First-error reduction: one 64-bit atomicMin per warp,
         // skipped when a smaller offset is already recorded.
-        const unsigned long long pos = static_cast<unsigned long long>(d.rel) + werr;
-        unsigned long long *tgt = &ws->errkey;
-        if (pos < *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMin(tgt, pos);
+        const unsigned long long inv = ~(static_cast<unsigned long long>(d.rel) + werr);
+        unsigned long long *tgt = &ws->errinv;
+        if (inv > *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMax(tgt, inv);
         __threadfence();
       }
     }
@@ -346,8 +347,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const unsigned prev = atomicAdd(&ws->done, 1u);
     if (prev == gridDim.x - 1) {
       __threadfence();
-      const unsigned long long e = atomicOr(&ws->errkey, 0ull);
-      const StreamResult R = finish_stream(in, m, out, e == ~0ull ? -1 : static_cast<int64_t>(e),
+      const unsigned long long e = atomicOr(&ws->errinv, 0ull);
+      const StreamResult R = finish_stream(in, m, out, e == 0ull ? -1 : static_cast<int64_t>(~e),
                                            final_shard != 0, flags);
       res->out_len = R.out_len;
       res->err_pos = R.err_pos;
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         key[0] = shard_key(R.status, R.err_pos, shard_begin);
         key[1] = R.out_len;
       }
-      ws->errkey = ~0ull;
+      ws->errinv = 0ull;
       ws->done = 0;
       // (no system-scope fence: kernel completion makes these writes --
       // device or mapped host memory -- visible to the synchronizing host)
@@ -531,7 +532,7 @@ StreamWs *stream_ws(int dev, cudaStream_t stream) {
   if (it != g_ws.end()) return &it->second;
   StreamWs w;
   if (cudaMalloc(&w.d_ws, sizeof(DecWs)) != cudaSuccess) return nullptr;
-  DecWs init{~0ull, 0u, 0u};
+  DecWs init{0ull, 0u, 0u};
   if (cudaMemcpy(w.d_ws, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
   if (cudaHostAlloc(&w.h_res, sizeof(b64_result), cudaHostAllocMapped) != cudaSuccess) return nullptr;
   if (cudaHostGetDevicePointer(&w.d_res, w.h_res, 0) != cudaSuccess) return nullptr;
@@ -735,6 +736,16 @@ int b64_decode_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, b64_result 
 int b64_decode_ex_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
                         b64_result *d_result, b64_stream_t stream) {
   return decode_shard_ex(d_in, m, 1, d_out, flags, d_result, stream);
+}
+
+int b64_decode_scratch_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags,
+                             b64_result *d_result, void *d_scratch, b64_stream_t stream) {
+  if (m < 0 || !flags_ok(flags) || d_result == nullptr || d_scratch == nullptr ||
+      (reinterpret_cast<uintptr_t>(d_scratch) & 7) != 0 || (m > 0 && d_in == nullptr) ||
+      (b64_decoded_max_len_ex(m, flags) > 0 && d_out == nullptr))
+    return B64_ERR_ARG;
+  DevGuard g(stream);
+  return decode_launch(d_in, m, 1, d_out, d_result, stream, static_cast<DecWs *>(d_scratch), flags);
 }
 
 int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flags, int64_t *out_len,

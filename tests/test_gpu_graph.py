@@ -80,3 +80,44 @@ def test_graph_replay_ws_decode_and_batch():
         rr = host(raw)
         for i in range(lens.size):
             assert np.array_equal(o[oo[i]:oo[i + 1]], oracle.encode(rr[off[i]:off[i + 1]])), i
+
+
+def test_graphs_with_own_scratch_replay_concurrently():
+    """two decode graphs captured on the SAME stream, each with its
+    own caller-owned scratch record (b64_decode_scratch_async), replayed at
+    the same time on two streams -- one on clean text, one on text with an
+    error: each result record is its own input's (the library's per-stream
+    scratch would be shared between them)."""
+    n = 3 << 20
+    x = torch.from_numpy(splitmix_bytes(601, 0, n)).to(DEV)
+    t = b64.b64_encode(x)
+    td = t.clone()
+    td[123_457] = ord("!")
+    ya = torch.empty(b64.b64_decoded_max_len(t.numel()), dtype=torch.uint8, device=DEV)
+    yb = torch.empty_like(ya)
+    ra, rb = b64.result_tensor(DEV), b64.result_tensor(DEV)
+    sa, sb = b64.scratch_tensor(DEV), b64.scratch_tensor(DEV)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        b64.b64_decode_scratch_async(t, ya, ra, sa, stream=s)
+        b64.b64_decode_scratch_async(td, yb, rb, sb, stream=s)
+    torch.cuda.synchronize()
+    ga, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(ga, stream=s):
+        b64.b64_decode_scratch_async(t, ya, ra, sa, stream=s)
+    with torch.cuda.graph(gb, stream=s):
+        b64.b64_decode_scratch_async(td, yb, rb, sb, stream=s)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(20):
+        ra.zero_()
+        rb.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            ga.replay()
+        with torch.cuda.stream(s2):
+            gb.replay()
+        torch.cuda.synchronize()
+        assert b64.unpack_result(ra)[:3] == (n, -1, 0)
+        assert b64.unpack_result(rb)[:3] == (3 * (123_457 // 4), 123_457, b64.B64_ERR_INVALID_CHAR)
+    assert torch.equal(ya[:n], x)
+    assert int(sa.abs().sum().item()) == 0 and int(sb.abs().sum().item()) == 0  # left zero
