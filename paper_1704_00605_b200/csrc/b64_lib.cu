@@ -272,6 +272,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t chars = 4 * (m / 4);
   const bool pad_rules = final_shard != 0 && (m % 4) == 0;
+  // A single-CTA launch (inputs of one tile) reduces its error offset in
+  // shared memory and finishes without the global done count: no device-
+  // scope atomics or fences on the latency-bound small-input path.
+  const bool solo = gridDim.x == 1;
+  __shared__ unsigned long long s_errinv;
 
   // Inverse map A: invalid everywhere, then A(B(v)) = v.
   if (tid < 256) g_dec_tab[tid] = kInvalid;
@@ -281,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       mbar_init(&S.empty[s], kWarpsC);
     }
     fence_mbar_init();
+    s_errinv = 0ull;
   }
   __syncthreads();
   if (tid < 64) g_dec_tab[ascii_of(tid, flags)] = static_cast<uint8_t>(tid);
@@ -325,9 +331,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         // First-error reduction: one 64-bit atomicMin per warp,
         // skipped when a smaller offset is already recorded.
         const unsigned long long inv = ~(static_cast<unsigned long long>(d.rel) + werr);
-        unsigned long long *tgt = &ws->errinv;
-        if (inv > *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMax(tgt, inv);
-        __threadfence();
+        if (solo) {
+          atomicMax(&s_errinv, inv);
+        } else {
+          unsigned long long *tgt = &ws->errinv;
+          if (inv > *reinterpret_cast<volatile unsigned long long *>(tgt)) atomicMax(tgt, inv);
+          __threadfence();
+        }
       }
     }
     if (direct) continue;
@@ -343,11 +353,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   // barrier orders every warp's error atomics before the done count.
   named_bar_sync(1, kNT);
   if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&ws->done, 1u);
-    if (prev == gridDim.x - 1) {
+    unsigned prev = 0;
+    if (!solo) {
       __threadfence();
-      const unsigned long long e = atomicOr(&ws->errinv, 0ull);
+      prev = atomicAdd(&ws->done, 1u);
+    }
+    if (solo || prev == gridDim.x - 1) {
+      unsigned long long e = s_errinv;
+      if (!solo) {
+        __threadfence();
+        e = atomicOr(&ws->errinv, 0ull);
+      }
       const StreamResult R = finish_stream(in, m, out, e == 0ull ? -1 : static_cast<int64_t>(~e),
                                            final_shard != 0, flags);
       res->out_len = R.out_len;
@@ -359,8 +375,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         key[0] = shard_key(R.status, R.err_pos, shard_begin);
         key[1] = R.out_len;
       }
-      ws->errinv = 0ull;
-      ws->done = 0;
+      if (!solo) {
+        ws->errinv = 0ull;
+        ws->done = 0;
+      }
       // (no system-scope fence: kernel completion makes these writes --
       // device or mapped host memory -- visible to the synchronizing host)
     }

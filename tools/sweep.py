@@ -182,6 +182,7 @@ VARIANTS = {
     "b_p8_skel": {"B64_BATCH_PASSES": 8, "B64_BATCH_WARPS": 8, "B64_SKELETON": 1},
     # one-pass compaction (f3 / f4 general path)
     "cp_onepass": {"B64_CP_ONEPASS": 1},
+    "base_ref": {},
     "op_s7_l3": {"B64_CP_ONEPASS": 1, "B64_OP_SLOTS": 7, "B64_OP_LAG": 3},
     "op_s8_l5": {"B64_CP_ONEPASS": 1, "B64_OP_SLOTS": 8, "B64_OP_LAG": 5},
     "op_s6_l2": {"B64_CP_ONEPASS": 1, "B64_OP_SLOTS": 6, "B64_OP_LAG": 2},
