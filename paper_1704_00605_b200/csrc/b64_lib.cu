@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
 // ------------------------------------------------------ decode kernel ---
 // Single buffer / shard (rows a6-a12).
-template <int IA, int OA, int P = kSinglePasses>
+template <int IA, int OA, int P = kSinglePasses, bool SOLO = false>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
                   int64_t ntiles, int final_shard, DecWs *ws, b64_result *res, int flags,
@@ -272,10 +272,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t chars = 4 * (m / 4);
   const bool pad_rules = final_shard != 0 && (m % 4) == 0;
-  // A single-CTA launch (inputs of one tile) reduces its error offset in
-  // shared memory and finishes without the global done count: no device-
-  // scope atomics or fences on the latency-bound small-input path.
-  const bool solo = gridDim.x == 1;
+  // SOLO: a single-CTA launch (inputs of one tile) reduces its error offset
+  // in shared memory and finishes without the global done count: no device-
+  // scope atomics or fences on the latency-bound small-input path.  (A
+  // separate instantiation: the multi-CTA kernels keep their exact code.)
+  constexpr bool solo = SOLO;
   __shared__ unsigned long long s_errinv;
 
   // Inverse map A: invalid everywhere, then A(B(v)) = v.
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       mbar_init(&S.empty[s], kWarpsC);
     }
     fence_mbar_init();
-    s_errinv = 0ull;
+    if (solo) s_errinv = 0ull;
   }
   __syncthreads();
   if (tid < 64) g_dec_tab[ascii_of(tid, flags)] = static_cast<uint8_t>(tid);
@@ -454,6 +455,11 @@ DecFn dec_small_table[3][3] = {
     {decode_kernel<4, 16, SP>, decode_kernel<4, 4, SP>, decode_kernel<4, 1, SP>},
     {decode_kernel<1, 16, SP>, decode_kernel<1, 4, SP>, decode_kernel<1, 1, SP>},
 };
+DecFn dec_solo_table[3][3] = {
+    {decode_kernel<16, 16, SP, true>, decode_kernel<16, 4, SP, true>, decode_kernel<16, 1, SP, true>},
+    {decode_kernel<4, 16, SP, true>, decode_kernel<4, 4, SP, true>, decode_kernel<4, 1, SP, true>},
+    {decode_kernel<1, 16, SP, true>, decode_kernel<1, 4, SP, true>, decode_kernel<1, 1, SP, true>},
+};
 constexpr size_t kEncRingBytes = sizeof(EncRing) * kBWarps;
 constexpr size_t kDecRingBytes = sizeof(DecRing) * kBWarps;
 
@@ -481,6 +487,9 @@ DevInfo *device_setup_info(int *dev_out) {
       for (auto f : row)
         if (set_smem(f, sizeof(EncSmemP<kSmallPasses>)) != cudaSuccess) return nullptr;
     for (auto &row : dec_small_table)
+      for (auto f : row)
+        if (set_smem(f, sizeof(DecSmemP<kSmallPasses>)) != cudaSuccess) return nullptr;
+    for (auto &row : dec_solo_table)
       for (auto f : row)
         if (set_smem(f, sizeof(DecSmemP<kSmallPasses>)) != cudaSuccess) return nullptr;
     if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return nullptr;
@@ -610,7 +619,8 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
   const bool small = kSmallPasses != kSinglePasses && ntiles < 2 * static_cast<int64_t>(sms);
   if (small) ntiles = (chars + DecG<kSmallPasses>::kIn - 1) / DecG<kSmallPasses>::kIn;
   const int64_t grid = grid_for(ntiles, sms);
-  DecFn f = (small ? dec_small_table : dec_table)[align_class(d_in)][align_class(d_out)];
+  DecFn f = (small ? (grid == 1 ? dec_solo_table : dec_small_table) : dec_table)[align_class(d_in)]
+                                                                              [align_class(d_out)];
   const size_t smem = small ? sizeof(DecSmemP<kSmallPasses>) : sizeof(DecSmem);
   f<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(d_in, m, d_out, ntiles, final_shard, ws,
                                                              d_result, flags, shard_begin, d_key);
