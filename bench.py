@@ -395,6 +395,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel", "achieved": ach, "peak": hbm,
                          "unit": "GB/s", "frac": ach / hbm, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": hbm_src,
+                         "frac_of_nominal_8tbs": ach / 8000.0,
                          "algorithmic_bytes_per_launch": dec_bytes if dom == "decode" else enc_bytes},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (2 if world == 1 else 3) * K,
             "gpu_launches_scope": "per rank: 1 encode_kernel + 1 decode_kernel per step" + (
