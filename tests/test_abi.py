@@ -94,3 +94,26 @@ def test_wrapped_len_matches_oracle_and_rejects_bad_lines():
                         oracle._load().oracle_encoded_len_wrapped(n, L, crlf, fl)
     for bad in (0, 3, 6, 77, 16388):
         assert b64.b64_encoded_len_wrapped(10, bad, True, 0) == b64.B64_ERR_ARG
+
+
+def test_shard_key_and_combine_host():
+    """The multi-GPU exchange arithmetic of the C ABI (pure host): the key
+    packs a global offset with its status, the MIN over shards picks the
+    first error, and the combine follows Alg 2's output rule."""
+    INT64_MAX = b64.INT64_MAX
+    assert b64.b64_shard_key(0, -1, 123) == INT64_MAX
+    assert b64.b64_shard_key(1, 5, 100) == (105 << 2) | 1
+    assert b64.b64_shard_key(2, 8, 0) == (8 << 2) | 2
+    assert b64.b64_shard_key(3, 10, 4) == (14 << 2) | 3
+    # clean: lengths summed, pad count from the total length
+    assert b64.b64_combine_shards(INT64_MAX, [30, 30, 28], 120) == (0, -1, 88, 2)
+    assert b64.b64_combine_shards(INT64_MAX, [3], 6) == (0, -1, 3, 0)  # m % 4 != 0 (NOPAD tail)
+    # errors: the MIN key wins; out_len = 3 * floor(err / 4) for every status
+    keys = [b64.b64_shard_key(1, 7, 40), b64.b64_shard_key(3, 2, 80), INT64_MAX]
+    assert b64.b64_combine_shards(min(keys), [30, 30, 0], 120) == (1, 47, 33, 0)
+    assert b64.b64_combine_shards(b64.b64_shard_key(2, 4, 116), [87, 0], 121) == (2, 120, 90, 0)
+    assert b64.b64_combine_shards(b64.b64_shard_key(3, 3, 116), [87, 0], 120) == (3, 119, 87, 0)
+    lib = b64.load_library()
+    assert lib.b64_combine_shards(0, None, 1, 4, None) == b64.B64_ERR_ARG
+    assert lib.b64_combine_shards_async(None, None, 0, 4, None, None) == b64.B64_ERR_ARG
+    assert lib.b64_decode_scratch_async(None, 4, None, 0, None, None, None) == b64.B64_ERR_ARG
