@@ -499,8 +499,32 @@ def run_small_configs(args):
             b64.b64_encode(x, out=t, stream=gs)
             b64.b64_decode_async(t, y, res, stream=gs)
             b64.b64_decode_async(td, y, res2, stream=gs)
-        graph_ms = timed(graph.replay, "graph_replay")
+        serial_ms = timed(graph.replay, "graph_replay_serial")
         assert b64.unpack_result(res)[2] == 0 and b64.unpack_result(res2)[1] == pos
+        # the two decodes are independent once the encode is done: fork-join
+        # graph, the dirty decode on a second stream (its own output buffer;
+        # every stream has its own decode scratch)
+        gs2 = torch.cuda.Stream()
+        y2 = torch.empty_like(y)
+        with torch.cuda.stream(gs2):
+            b64.b64_decode_async(td, y2, res2, stream=gs2)
+        torch.cuda.synchronize(dev)
+        graph2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph2, stream=gs):
+            b64.b64_encode(x, out=t, stream=gs)
+            ev_f = torch.cuda.Event()
+            ev_f.record(gs)
+            gs2.wait_event(ev_f)
+            b64.b64_decode_async(t, y, res, stream=gs)
+            b64.b64_decode_async(td, y2, res2, stream=gs2)
+            ev_j = torch.cuda.Event()
+            ev_j.record(gs2)
+            gs.wait_event(ev_j)
+        res.zero_()
+        res2.zero_()
+        graph_ms = timed(graph2.replay, "graph_replay")
+        assert b64.unpack_result(res)[2] == 0 and b64.unpack_result(res)[0] == n
+        assert b64.unpack_result(res2)[1] == pos and torch.equal(y[:n], x)
         # end-to-end sync API latency (includes the result read-back)
         t0 = time.perf_counter()
         for _ in range(200):
@@ -514,10 +538,12 @@ def run_small_configs(args):
         detail = {"encode_us": enc_ms * 1e3, "decode_us": dec_ms * 1e3, "dirty_decode_us": dirty_ms * 1e3,
                   "encode_hot_l2_us": hot_enc * 1e3, "decode_hot_l2_us": hot_dec * 1e3,
                   "graph_replay_all_three_us": graph_ms * 1e3,
+                  "graph_replay_all_three_serial_us": serial_ms * 1e3,
                   "sync_decode_api_us": sync_us}
         dom, dom_ms = ("encode", enc_ms) if enc_ms >= dec_ms else ("decode", dec_ms)
         desc = ("C1: 2^20 random bytes (seed 0): encode, decode, decode of a copy with one NA191 byte; "
-                "step = one CUDA-graph replay of the three calls")
+                "step = one CUDA-graph replay of the three calls (the two decodes, independent once the "
+                "encode is done, on forked streams)")
         launches = 3
     elif wl == "c2":
         lens, _ = W.c2_lengths()
