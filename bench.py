@@ -603,9 +603,11 @@ def run_small_configs(args):
         desc = ("C2: 10,000 messages, log-uniform 100 B - 64 KiB (seed 1): batched encode + batched decode "
                 "(incl. planner); step = one CUDA-graph replay of the two calls")
         launches = 2
-    elif wl == "despace":
-        # f3: 1 GiB of MIME-style text (76-char lines + CRLF, 2.6 % whitespace),
+    elif wl in ("despace", "despace_irregular"):
+        # f3: 1.27 GB of MIME-style text (76-char lines + CRLF, 2.6 % whitespace),
         # built on the device from C3-seeded bytes with our encoder + a view.
+        # despace_irregular: every 50th line ends in " \n" instead of CR LF,
+        # so the line fast path gives up and the two-pass path does the work.
         nraw = 57 * (1 << 24)
         raw = torch.empty(nraw, dtype=torch.uint8, device=dev)
         fill(raw, W.C3_SEED)
@@ -616,6 +618,8 @@ def run_small_configs(args):
         w[:, :76] = lines
         w[:, 76] = 13
         w[:, 77] = 10
+        if wl == "despace_irregular":
+            w[::50, 76] = ord(" ")
         w = w.view(-1)
         m = w.numel()
         out = torch.empty(m, dtype=torch.uint8, device=dev)
@@ -628,15 +632,19 @@ def run_small_configs(args):
         ds_ms = timed(ds, "despace")
         kept = int(olen_t[0].item())
         assert kept == t.numel() and torch.equal(out[:kept], t)
+        fast = int(ws[:4].view(torch.int32).item())  # WlState.verdict
+        assert fast == (1 if wl == "despace" else 0)
         ms = ds_ms
         value = m / (ms / 1e3) / 1e9
         algo = {"despace": m + kept}
         detail = {"despace_ms": ds_ms, "in_bytes": m, "out_bytes": kept,
-                  "despace_GBps_input": m / (ds_ms / 1e3) / 1e9}
+                  "despace_GBps_input": m / (ds_ms / 1e3) / 1e9,
+                  "path": "line fast path" if fast else "general two-pass path (fast path gave up)"}
         dom, dom_ms = "despace", ds_ms
         kname = {"despace": "b64_despace call (all its kernels)"}
-        desc = "f3: whitespace removal of 1.27 GB MIME-style text (76-char lines + CRLF)"
-        launches = 2
+        desc = ("f3: whitespace removal of 1.27 GB MIME-style text (76-char lines + CRLF)"
+                + (", irregular line ends (general path)" if wl == "despace_irregular" else ""))
+        launches = 3
     elif wl == "mime":
         # f4: MIME round trip of 57 * 2^24 random bytes: line-wrapped encode
         # (76-char lines + CRLF, 1.31 GB of text) and whitespace-tolerant
@@ -827,7 +835,7 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c5", "c3", "c1", "c2", "c4", "despace", "mime", "mime_irregular", "sweep"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c3", "c1", "c2", "c4", "despace", "despace_irregular", "mime", "mime_irregular", "sweep"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-bytes", type=int, default=3 << 28)
@@ -848,7 +856,7 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload in ("c1", "c2", "c4", "despace", "mime", "mime_irregular", "sweep"):
+    elif args.workload in ("c1", "c2", "c4", "despace", "despace_irregular", "mime", "mime_irregular", "sweep"):
         if args.gpus != 1:
             raise SystemExit(f"--workload {args.workload} is a single-GPU parity config; use c5 or c3 for --gpus > 1")
         run_small_configs(args)

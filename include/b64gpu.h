@@ -240,10 +240,17 @@ int b64_decode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
 /* Appendix B: remove ' ' (0x20), '\n' (0x0A) and '\r' (0x0D)
  * from d_in[0..m) into d_out (capacity m; d_out must not overlap d_in),
  * preserving order; *d_out_len (device int64) receives the new length.
- * Two kernels: per-chunk kept counts, then per-chunk compaction of 16 KiB
- * TMA-staged tiles (warp scans, congruent 16-byte copy-out) at the chunk
- * offsets.  d_ws: b64_despace_workspace_bytes(m) bytes of
- * device memory.  Asynchronous. */
+ * Three kernels.  (1) A verified fast path for line-structured text (MIME /
+ * PEM: lines of L chars, L a multiple of 4 up to 4092, each ending in the
+ * same EOL, "\n" or "\r\n", the last line shorter and its EOL optional):
+ * one strided copy of the lines' characters; any byte below 0x21 inside a
+ * line or any deviation from the structure makes it give up (its writes to
+ * d_out are then overwritten).  (2)-(3) Otherwise the general path:
+ * per-chunk kept counts, then per-chunk compaction of 16 KiB TMA-staged
+ * tiles (warp scans, congruent 16-byte copy-out) at the chunk offsets; both
+ * return at once when (1) succeeded.  The result is the same either way.
+ * d_ws: b64_despace_workspace_bytes(m) bytes of device memory, 16-byte
+ * aligned.  Asynchronous. */
 size_t b64_despace_workspace_bytes(int64_t m);
 int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_len, void *d_ws,
                 size_t ws_bytes, b64_stream_t stream);

@@ -399,7 +399,8 @@ struct alignas(128) DsSmem {
 __global__ void __launch_bounds__(kCpThreads, kCpCtasPerSm)
     despace_kernel(const uint8_t *__restrict__ in, int64_t m, uint8_t *__restrict__ out,
                    const int64_t *__restrict__ counts, const uint32_t *__restrict__ masks,
-                   int64_t tpc, int64_t *out_len) {
+                   int64_t tpc, int64_t *out_len, const int32_t *skip = nullptr) {
+  if (skip != nullptr && *skip == 1) return;  // the line-structured fast path already wrote it
   extern __shared__ __align__(128) uint8_t smem_raw[];
   DsSmem &S = *reinterpret_cast<DsSmem *>(smem_raw);
   const int tid = threadIdx.x;

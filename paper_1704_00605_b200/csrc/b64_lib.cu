@@ -37,6 +37,9 @@
 #if B64_CP_ONEPASS
 #include "b64_onepass.cuh"
 #endif
+namespace b64 {
+constexpr size_t kDsHdrBytes = 64;  // despace workspace: WlState of the line fast path
+}
 
 namespace b64 {
 
@@ -398,6 +401,7 @@ using namespace b64;
 struct DevInfo {
   int sms = 0;
   int wl_ctas = 1;  // resident decode_lines_kernel CTAs per SM
+  int dl_ctas = 1;  // resident despace (line fast path) CTAs per SM
   int op_ctas = 1;   // resident one-pass compaction CTAs per SM
   bool attrs_set = false;
 };
@@ -495,11 +499,16 @@ DevInfo *device_setup_info(int *dev_out) {
     if (set_smem(batch_kernel<false>, kEncRingBytes) != cudaSuccess) return nullptr;
     if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return nullptr;
     if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return nullptr;
-    if (set_smem(decode_lines_kernel, sizeof(WlSmem)) != cudaSuccess) return nullptr;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.wl_ctas, decode_lines_kernel, kWlThreads,
-                                                      sizeof(WlSmem)) != cudaSuccess ||
+    if (set_smem(decode_lines_kernel<false>, sizeof(WlSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(decode_lines_kernel<true>, sizeof(WlSmem)) != cudaSuccess) return nullptr;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.wl_ctas, decode_lines_kernel<false>,
+                                                      kWlThreads, sizeof(WlSmem)) != cudaSuccess ||
         di.wl_ctas < 1)
       di.wl_ctas = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.dl_ctas, decode_lines_kernel<true>,
+                                                      kWlThreads, sizeof(WlSmem)) != cudaSuccess ||
+        di.dl_ctas < 1)
+      di.dl_ctas = 1;
     if (set_smem(encode_wrap_kernel<2, true>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
     if (set_smem(encode_wrap_kernel<2, false>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
     if (set_smem(encode_wrap_kernel<1, false>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
@@ -1031,7 +1040,8 @@ size_t b64_despace_workspace_bytes(int64_t m) {
 #if B64_CP_ONEPASS
   return 4 * static_cast<size_t>((15 + m + kCpTile - 1) / kCpTile);  // per-tile kept counts
 #else
-  return 8 * kCpMaxChunks + cp_mask_bytes(m);  // per-chunk kept counts + keep masks
+  // line fast path state | per-chunk kept counts | keep masks
+  return kDsHdrBytes + 8 * kCpMaxChunks + cp_mask_bytes(m);
 #endif
 }
 
@@ -1059,12 +1069,20 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
 #else
   int64_t ntiles, tpc, grid;
   cp_plan(d_in, m, di->sms, &ntiles, &tpc, &grid);
-  int64_t *counts = static_cast<int64_t *>(d_ws);
-  uint32_t *masks = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(d_ws) + 8 * kCpMaxChunks);
+  uint8_t *base = static_cast<uint8_t *>(d_ws);
+  WlState *wl = reinterpret_cast<WlState *>(base);
+  int64_t *counts = reinterpret_cast<int64_t *>(base + kDsHdrBytes);
+  uint32_t *masks = reinterpret_cast<uint32_t *>(base + kDsHdrBytes + 8 * kCpMaxChunks);
+  // 1. verified fast path for line-structured text (MIME / PEM): a strided
+  // copy with the line structure checked; 2-3. the general two-pass path,
+  // whose kernels return at once when 1. succeeded.
+  if (cudaMemsetAsync(wl, 0, sizeof(WlState), stream) != cudaSuccess) return B64_ERR_CUDA;
+  decode_lines_kernel<true><<<static_cast<unsigned>(di->sms * di->dl_ctas), kWlThreads, sizeof(WlSmem),
+                              stream>>>(d_in, m, d_out, wl, nullptr, 0, d_out_len);
   cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(d_in, m, tpc, counts,
-                                                                          masks, nullptr);
+                                                                          masks, nullptr, &wl->verdict);
   despace_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(DsSmem), stream>>>(
-      d_in, m, d_out, counts, masks, tpc, d_out_len);
+      d_in, m, d_out, counts, masks, tpc, d_out_len, &wl->verdict);
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 #endif
 }
@@ -1107,8 +1125,8 @@ int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
     return B64_ERR_CUDA;
   // 1. verified fast path for line-structured text (MIME / PEM); 2. the
   // general one-pass kernel, which returns at once when 1. succeeded.
-  decode_lines_kernel<<<static_cast<unsigned>(sms * di->wl_ctas), kWlThreads, sizeof(WlSmem), stream>>>(
-      d_in, m, d_out, wl, d_result, flags);
+  decode_lines_kernel<false><<<static_cast<unsigned>(sms * di->wl_ctas), kWlThreads, sizeof(WlSmem), stream>>>(
+      d_in, m, d_out, wl, d_result, flags, nullptr);
   if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
   return op_launch(decode_ws1_kernel, ntiles, di, sizeof(OpWsSmem), stream, d_in, m, d_out,
                    reinterpret_cast<uint32_t *>(base + kWsHdrBytes), reinterpret_cast<OpWsHdr *>(base),
@@ -1123,8 +1141,8 @@ int b64_decode_ws_async(const uint8_t *d_in, int64_t m, uint8_t *d_out, int flag
   // 1. verified fast path for line-structured text (MIME / PEM); 2-3. the
   // general path, which returns at once when 1. succeeded.
   if (cudaMemsetAsync(wl, 0, sizeof(WlState), stream) != cudaSuccess) return B64_ERR_CUDA;
-  decode_lines_kernel<<<static_cast<unsigned>(sms * di->wl_ctas), kWlThreads, sizeof(WlSmem), stream>>>(
-      d_in, m, d_out, wl, d_result, flags);
+  decode_lines_kernel<false><<<static_cast<unsigned>(sms * di->wl_ctas), kWlThreads, sizeof(WlSmem), stream>>>(
+      d_in, m, d_out, wl, d_result, flags, nullptr);
   cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(
       d_in, m, tpc, counts, masks, &hdr->errkey, &wl->verdict);
   decode_ws_kernel<<<static_cast<unsigned>(grid), kCpThreads, sizeof(WsSmem), stream>>>(

@@ -74,9 +74,25 @@ struct alignas(128) WlSmem {
   int32_t flag;
 };
 
+// Any byte of w below 0x21 (' ', '\n', '\r' and the other control bytes):
+// the classic "has less than" SWAR test, exact as an any-test for bytes
+// < 0x80 (bytes >= 0x80 never match).
+__device__ __forceinline__ bool has_below_0x21(uint32_t w) {
+  return ((w - 0x21212121u) & ~w & 0x80808080u) != 0u;
+}
+
+// DS = false: the verified line-structured fast path of b64_decode_ws.
+// DS = true: the same for b64_despace (Appendix B on MIME / PEM text): every
+// quad of kept characters is copied to out + 4 q (a quad never straddles a
+// line, L being a multiple of 4) with one coalesced 4-byte store per lane;
+// a byte below 0x21 inside a line (white space, or a control byte despace
+// would keep) is a violation, like a bad EOL, and the general two-pass path
+// (cp_mask_kernel + despace_kernel) then produces the output.  On success
+// *ds_out_len = the kept length.
+template <bool DS>
 __global__ void __launch_bounds__(kWlThreads, 1)
     decode_lines_kernel(const uint8_t *__restrict__ in, int64_t M, uint8_t *__restrict__ out,
-                        WlState *st, b64_result *res, int flags) {
+                        WlState *st, b64_result *res, int flags, int64_t *ds_out_len) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   WlSmem &S = *reinterpret_cast<WlSmem *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -216,16 +232,49 @@ __global__ void __launch_bounds__(kWlThreads, 1)
           const int qb = qa + per < nq ? qa + per : nq;
           const int imis = static_cast<int>((reinterpret_cast<uintptr_t>(in) + static_cast<uintptr_t>(src)) & 15);
           const uint32_t *win = reinterpret_cast<const uint32_t *>(S.in[s]);
-          uint8_t *gdst = out + 3 * (q0 + qa);
+          uint8_t *gdst = out + (DS ? 4 : 3) * (q0 + qa);
           const int omis = static_cast<int>(reinterpret_cast<uintptr_t>(gdst) & 15);
           uint8_t *ob = slice + omis - 3 * qa;  // quad q -> ob + 3q
           uint32_t bad = 0;
           const bool interior = q1 < Q && (line0 + Lt) * static_cast<int64_t>(Sl) <= M;
+          const bool direct = !DS && kWlDirect && interior && ((reinterpret_cast<uintptr_t>(gdst) & 3) == 0);
+          if constexpr (DS) {
+            // despace: each lane copies quads q = qa + lane + 32 i (the EOL
+            // of every line is checked below); 4-byte aligned destination:
+            // one coalesced STG.32 per quad, else byte stores
+            const bool al4 = (reinterpret_cast<uintptr_t>(gdst) & 3) == 0;
+            if (qa < qb) {
+              int q = qa + lane;
+              int ln = line_of(q), col = q - ln * G;
+              int a = imis + ln * Sl + 4 * col;
+              uint32_t *gw = reinterpret_cast<uint32_t *>(gdst) + lane;
+              for (; q < qb; q += 32) {
+                const uint32_t w = __funnelshift_r(win[a >> 2], win[(a >> 2) + 1], 8 * (a & 3));
+                if (has_below_0x21(w)) bad |= 0x80u;
+                if (al4) {
+                  *gw = w;
+                } else {
+                  uint8_t *p = gdst + 4 * (q - qa);
+                  p[0] = static_cast<uint8_t>(w);
+                  p[1] = static_cast<uint8_t>(w >> 8);
+                  p[2] = static_cast<uint8_t>(w >> 16);
+                  p[3] = static_cast<uint8_t>(w >> 24);
+                }
+                gw += 32;
+                a += pstep;
+                col += dc32;
+                if (col >= G) {
+                  col -= G;
+                  a += e;
+                }
+              }
+            }
+          }
+          if constexpr (!DS) {
           // DIRECT (B64_WL_DIRECT, 4-byte aligned output): interior warps pack
           // 32 lanes' 3-byte results into 24 words with two shuffles and write
           // them with one coalesced 4-byte store per lane -- no staging slice,
           // no copy-out (3 STS.U8 + 0.75 LDS.128 per 32 quads -> 2 SHFL)
-          const bool direct = kWlDirect && interior && ((reinterpret_cast<uintptr_t>(gdst) & 3) == 0);
           if (direct && qa < qb) {
             int q = qa + lane;
             int ln = line_of(q), col = q - ln * G;
@@ -384,6 +433,7 @@ __global__ void __launch_bounds__(kWlThreads, 1)
               p[2] = static_cast<uint8_t>(V);
             }
           }
+          }  // !DS
           // EOL of every line whose last quad this warp owns (and that has one)
           for (int ln = line_of(qa) + lane, lb = line_of(qb); ln < lb; ln += 32) {
             if ((line0 + ln + 1) * Sl > M) break;
@@ -396,7 +446,7 @@ __global__ void __launch_bounds__(kWlThreads, 1)
               S.flag = 1;
               atomicExch(&st->viol, 1);
             }
-          } else if (qa < qb && !direct) {
+          } else if (!DS && qa < qb && !direct) {
             // this warp's bytes: congruent staging -> 16-byte stores + byte edges
             __syncwarp();
             const int n = 3 * (qb - qa);
@@ -449,6 +499,12 @@ __global__ void __launch_bounds__(kWlThreads, 1)
       st->verdict = 0;
       return;
     }
+  if constexpr (DS) {  // the partial final quad's chars, then the length
+    for (int64_t i = Mc & ~static_cast<int64_t>(3); i < Mc; ++i) out[i] = in[(i / Lr) * Sr + i % Lr];
+    *ds_out_len = Mc;
+    st->verdict = 1;
+    return;
+  }
   const StreamResult R = finish_stream_at(
       [in, Lr, Sr](int64_t i) -> uint32_t { return in[(i / Lr) * Sr + i % Lr]; }, Mc, out, -1,
       true, flags);

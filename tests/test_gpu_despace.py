@@ -74,3 +74,88 @@ def test_despace_then_decode_wrapped_text():
     n = int(olen.item())
     y, st, ep = b64.b64_decode(d[:n])
     assert (st, ep) == (0, -1) and np.array_equal(host(y), x)
+
+
+# ---- line-structured fast path (MIME / PEM text): one strided copy with the
+# line structure verified; anything else falls back to the two-pass path.
+# The verdict word sits at the start of the workspace (WlState.verdict).
+
+def despace_with_verdict(w, im=0, om=0):
+    lib = b64.load_library()
+    ws = torch.empty(lib.b64_despace_workspace_bytes(w.size) + 256, dtype=torch.uint8, device=DEV)
+    base, out = empty_dev(max(w.size, 1), om)
+    o, olen = b64.b64_despace(to_dev(w, im), out=out, ws=ws)
+    n = int(olen.item())
+    g = host(base)
+    assert (g[:om] == 0xCC).all() and (g[om + max(w.size, 1):] == 0xCC).all(), "guard bytes"
+    verdict = int(ws[:4].view(torch.int32).item()) if w.size else 1
+    return host(o)[:n], verdict
+
+
+def wrapped(n, seed, line=76, crlf=True, final_eol=True):
+    w = oracle.encode_wrapped(splitmix_bytes(seed, 0, n), line, crlf=crlf)
+    if not final_eol and w.size:
+        w = w[: w.size - (2 if crlf else 1)]
+    return w
+
+
+def test_lines_fast_path_sizes():
+    for n in [1, 2, 3, 56, 57, 58, 57 * 20, 12_285, 12_300, 300_001, 3_600_000]:
+        for line, crlf in ((76, True), (64, False), (4, True), (4092, False)):
+            for fe in (True, False):
+                w = wrapped(n, 310 + n % 11, line, crlf, fe)
+                got, v = despace_with_verdict(w)
+                assert np.array_equal(got, oracle.despace(w)), (n, line, crlf, fe)
+                # text without any EOL (one line, no final EOL) has no line
+                # structure to detect: the general path handles it
+                assert v == int((w == 10).any()), (n, line, crlf, fe)
+
+
+def test_lines_fast_path_large_and_aligned():
+    w = wrapped(57 * (1 << 18) + 5, 311)  # many tiles per CTA, short final line
+    ref = oracle.despace(w)
+    for im, om in ((0, 0), (1, 0), (0, 3), (7, 13)):
+        got, v = despace_with_verdict(w, im, om)
+        assert v == 1 and np.array_equal(got, ref), (im, om)
+
+
+@pytest.mark.parametrize("kind", ["space_in_line", "tab", "ctrl", "extra_eol", "missing_eol", "bad_eol",
+                                  "trailing_space", "lf_in_crlf", "first_line_space", "line_not_mult4"])
+def test_lines_fast_path_falls_back(kind):
+    """Text that is not line-structured (or has a byte < 0x21 inside a line)
+    gives the plain Appendix B result through the general path."""
+    w = wrapped(300_000, 312)
+    b = bytearray(w.tobytes())
+    mid = 78 * 1500 + 30
+    if kind == "space_in_line":
+        b[mid] = 0x20
+    elif kind == "tab":
+        b[mid] = 0x09          # kept by Appendix B: must survive
+    elif kind == "ctrl":
+        b[mid] = 0x01
+    elif kind == "extra_eol":
+        b[mid:mid] = b"\r\n"
+    elif kind == "missing_eol":
+        del b[78 * 1500 + 76: 78 * 1500 + 78]
+    elif kind == "bad_eol":
+        b[78 * 1500 + 76] = ord(" ")
+    elif kind == "trailing_space":
+        b[-2:-2] = b" "
+    elif kind == "lf_in_crlf":
+        b[78 * 1500 + 76] = ord("\n")
+    elif kind == "first_line_space":
+        b[10] = 0x20
+    elif kind == "line_not_mult4":
+        b = bytearray(b"\r\n".join(bytes(w[i: i + 75]) for i in range(0, 75 * 100, 75)))
+    x = np.frombuffer(bytes(b), dtype=np.uint8).copy()
+    got, v = despace_with_verdict(x)
+    assert np.array_equal(got, oracle.despace(x)), kind
+    assert v == 0, kind
+
+
+def test_lines_fast_path_tail_cases():
+    w = wrapped(57 * 300 + 2, 313)  # partial final quad ('=' pad) on a short final line
+    for tail in (b"", b"\r\n", b" ", b"\n", b"\r\n\r\n", b"A", b"AB\r\n"):
+        x = np.concatenate([w[:-2], np.frombuffer(tail, dtype=np.uint8)])
+        got, _ = despace_with_verdict(x)
+        assert np.array_equal(got, oracle.despace(x)), tail
