@@ -1,7 +1,7 @@
 #!/bin/bash
 # Despace line fast path: build, the despace / ws / fuzz tests, bench lines
 # (fast path and the general path), and (NCU=1) one ncu --set full capture of
-# decode_lines_kernel<true> on the despace workload.
+# decode_lines_kernel on NCU_W (default: despace).
 set -u
 T=${1:-dl}
 mkdir -p gpurun_out
@@ -13,5 +13,5 @@ for w in despace despace_irregular mime mime_irregular; do
 done
 if [ "${NCU:-0}" = "1" ]; then
   NCUF="ncu --set full --clock-control none --import-source on"
-  timeout 600 $NCUF -k regex:"decode_lines" -s 1 -c 1 -o gpurun_out/${T}_ncu_ds -f python bench.py --workload despace --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/${T}_ncu_ds.log 2>&1; echo "ncu ds rc=$?"
+  timeout 600 $NCUF -k regex:"${NCU_K:-decode_lines}" -s ${NCU_S:-1} -c 1 -o gpurun_out/${T}_ncu_${NCU_W:-despace} -f python bench.py --workload ${NCU_W:-despace} --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/${T}_ncu.log 2>&1; echo "ncu rc=$?"
 fi
