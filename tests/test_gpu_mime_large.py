@@ -2,7 +2,8 @@
 seeded bytes -> line-wrapped encode (76 + CRLF, 5.2 GB of text) ->
 whitespace-tolerant decode back, and despace of the same text -- each
 compared in full with the CPU oracle (streamed in chunks of whole lines);
-error offsets beyond 2^32 are exact."""
+despace's general path on the same text made irregular; error offsets
+beyond 2^32 are exact."""
 import numpy as np
 import pytest
 import torch
@@ -70,7 +71,21 @@ def test_mime_past_4gib():
         seen_y += ref_y.size
         seen_d += ref_d.size
     assert (seen_w, seen_y, seen_d) == (m, N, dl)
-    del y, d
+    # the same text with one CR past 2^32 turned into ' ' (still App. B
+    # white space, so the despaced text is unchanged) is no longer line-
+    # structured: despace takes its general two-pass path, whose result must
+    # equal the (oracle-checked) fast-path result
+    del y
+    cr = 78 * ((1 << 32) // 78 + 7) + 76
+    assert int(w[cr].item()) == 13
+    w[cr] = ord(" ")
+    ws = torch.empty(b64.load_library().b64_despace_workspace_bytes(m), dtype=torch.uint8, device=DEV)
+    d2 = torch.empty(m, dtype=torch.uint8, device=DEV)
+    _, dlen2 = b64.b64_despace(w, out=d2, ws=ws)
+    assert int(ws[:4].view(torch.int32).item()) == 0  # WlState.verdict: general path
+    assert int(dlen2.item()) == dl and torch.equal(d2[:dl], d[:dl])
+    w[cr] = 13
+    del d, d2, ws
     # exact first-error offsets past 2^32 (line structure: byte 78k+j, j < 76),
     # against the oracle on the text from a line boundary before the error
     for pos in [(1 << 32) + 78 * 5 + 3, m - 200]:

@@ -5,7 +5,7 @@
 # are deleted on the box), the C5 traffic and launch-list CSVs.
 set -u
 T=${1:-final}
-WORKLOADS="c1 c2 c3 c4 despace mime mime_irregular" bash tools/gpu_check.sh $T
+WORKLOADS="c1 c2 c3 c4 despace despace_irregular mime mime_irregular" bash tools/gpu_check.sh $T
 bash tools/gpu_profile_all.sh $T
 for r in gpurun_out/${T}_*.ncu-rep; do
   [ -f "$r" ] || continue

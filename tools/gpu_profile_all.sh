@@ -5,7 +5,7 @@
 #    BEFORE the default bench, so its roofline.traffic comes from this build
 #  * the default bench line and the launch list (gpu__time_duration) of the same command
 #  * ncu --set full of encode_kernel / decode_kernel on C3 (one launch each)
-#  * ncu --set full of the batched kernels on C2, the f3/f4 kernels (despace, mime workloads)
+#  * ncu --set full of the batched kernels on C2, the f3/f4 kernels (despace fast / general path, mime workloads)
 set -u
 T=${1:-r02}
 mkdir -p gpurun_out
@@ -30,14 +30,17 @@ $B2 > gpurun_out/${T}_c2plain.json 2>&1 && \
 $NCU -k regex:batch_kernel -s 4 -c 2 -o gpurun_out/${T}_batch_c2 -f $B2 > gpurun_out/${T}_ncu_c2.log 2>&1
 BD="python bench.py --workload despace --steps 1 --warmup 3"
 $BD > gpurun_out/${T}_dsplain.json 2>&1 && \
-$NCU -k regex:"cp_mask|despace" -s 4 -c 2 -o gpurun_out/${T}_despace -f $BD > gpurun_out/${T}_ncu_ds.log 2>&1
+$NCU -k regex:"decode_lines" -s 3 -c 1 -o gpurun_out/${T}_despace -f $BD > gpurun_out/${T}_ncu_ds.log 2>&1
+BDI="python bench.py --workload despace_irregular --steps 1 --warmup 3"
+$BDI > gpurun_out/${T}_dsirrplain.json 2>&1 && \
+$NCU -k regex:"cp_mask|despace_kernel" -s 4 -c 2 -o gpurun_out/${T}_despaceirr -f $BDI > gpurun_out/${T}_ncu_dsirr.log 2>&1
 BM="python bench.py --workload mime --steps 1 --warmup 3"
 $BM > gpurun_out/${T}_mimeplain.json 2>&1 && \
 $NCU -k regex:"encode_wrap|decode_lines" -s 6 -c 2 -o gpurun_out/${T}_mime -f $BM > gpurun_out/${T}_ncu_mime.log 2>&1
 BI="python bench.py --workload mime_irregular --steps 1 --warmup 3"
 $BI > gpurun_out/${T}_mimeirrplain.json 2>&1 && \
 $NCU -k regex:"cp_mask|decode_ws" -s 6 -c 2 -o gpurun_out/${T}_mimeirr -f $BI > gpurun_out/${T}_ncu_mimeirr.log 2>&1
-for w in c1 c2 c4 despace mime mime_irregular sweep; do
+for w in c1 c2 c4 despace despace_irregular mime mime_irregular sweep; do
   python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/${T}_bench_$w.json 2> gpurun_out/${T}_bench_$w.err
 done
 echo profile-all-done
