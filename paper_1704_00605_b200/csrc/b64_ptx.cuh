@@ -141,6 +141,16 @@ __device__ __forceinline__ uint4 lds128(const void *p) {
   return v;
 }
 
+// The same from a 32-bit shared-window address.
+__device__ __forceinline__ uint4 lds128_a(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(saddr)
+               : "memory");
+  return v;
+}
+
 // L2 eviction policies (createpolicy); streaming data is evict_first.
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

@@ -5,7 +5,10 @@
 // the last line holds 1..L characters, with or without the EOL; there is no
 // other white space.  Then the i-th kept character sits at original offset
 // (i / L)(L + e) + i mod L, so every quad is decoded straight from the
-// TMA-staged text -- no mask pass, no compaction.
+// TMA-staged text -- no mask pass, no compaction.  Interior tiles of short
+// lines (L <= 128) are decoded line-major (lm_lines: one lane per line, each
+// window word loaded once, output staged per block of lines); other tiles
+// flat (lanes take consecutive quads across line ends).
 //
 // The structure is an assumption each launch VERIFIES, never trusts: L and
 // the EOL come from the first line (read by every CTA), the tail from the
@@ -32,7 +35,7 @@ namespace b64 {
 constexpr int kWlWarps = B64_WL_WARPS;             // compute warps
 constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #ifndef B64_WL_TILE
-#define B64_WL_TILE 77824
+#define B64_WL_TILE 79872
 #endif
 #ifndef B64_WL_SLEEP  // producer back-off between empty-slot polls (ns); 0 = try_wait loop
 #define B64_WL_SLEEP 0
@@ -44,6 +47,21 @@ constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #define B64_WL_DIRECT 1
 #endif
 constexpr bool kWlDirect = B64_WL_DIRECT != 0;
+#ifndef B64_WL_LINEMAJOR  // interior tiles with L <= 128: one lane per line
+#define B64_WL_LINEMAJOR 1
+#endif
+constexpr bool kWlLineMajor = B64_WL_LINEMAJOR != 0;
+constexpr int kWlLmMaxG = 32;  // quads per line up to which the line-major path runs
+// Line-major lane -> line map: stride 1 (lane l: line l of a 32-line block)
+// or 2 (lane l: lines 2l and 2l + 1 of a 64-line block, two passes), per
+// (G, e) whichever gives fewer shared-memory bank conflicts on the staging
+// stores (lanes 3G or 6G bytes apart) and the window loads (L + e or
+// 2(L + e) bytes apart) -- from a bank simulation of both maps, bit
+// G - 1 + 32 (e - 1) set = stride 2 (G <= 19: 64 lines of staging fit).
+constexpr uint64_t kWlLmStride2 = 0x77f7800072620ull;
+__device__ __forceinline__ int lm_stride(int G, int e) {
+  return ((kWlLmStride2 >> (G - 1 + 32 * (e - 1))) & 1) ? 2 : 1;
+}
 #ifndef B64_WL_STAGES
 #define B64_WL_STAGES 2
 #endif
@@ -53,7 +71,8 @@ constexpr int kWlMaxLine = 4092;      // longest line the fast path takes
 // per-warp output slice: a warp owns a contiguous range of <= ceil(quads/16)
 // quads of a tile, rounded up to whole 32-quad rows
 constexpr int kWlWarpQuads = ((kWlTile / 4 + kWlWarps - 1) / kWlWarps + 31) / 32 * 32;
-constexpr int kWlSlice = 3 * kWlWarpQuads + 48;
+// (at least one 64-line line-major block of 57-byte lines + 16 B of misalignment)
+constexpr int kWlSlice = 3 * kWlWarpQuads + 48 > 3696 ? 3 * kWlWarpQuads + 48 : 3696;
 
 // Per-call state in the caller's workspace (zeroed by a 16-byte memset
 // before the launch).
@@ -79,6 +98,96 @@ struct alignas(128) WlSmem {
 // < 0x80 (bytes >= 0x80 never match).
 __device__ __forceinline__ bool has_below_0x21(uint32_t w) {
   return ((w - 0x21212121u) & ~w & 0x80808080u) != 0u;
+}
+
+// Line-major decode of P consecutive lines li0 .. li0 + P - 1 of a block
+// (first line l0 of the tile) by one lane, interleaved for ILP: each line's
+// quads are consecutive in the window (each word loaded once, one funnel
+// shift per quad), its 3G output bytes consecutive in the warp's staging
+// slice at om + 3 G li: every 4 quads give 3 stream words, stored as 3
+// aligned STS.32 funnel-shifted by the line's staging misalignment d; the
+// <= 3 bytes before the first / after the last aligned word are byte stores
+// from the first / last quad.  Bad characters and a wrong EOL set 0x80 in bad.
+template <int P>
+__device__ __forceinline__ void lm_lines(const uint32_t *win, uint8_t *slice, int imis, int Sl, int L,
+                                         int G, int om, int l0, int li0, uint32_t tb, uint32_t eolw,
+                                         uint32_t eolm, uint32_t &bad) {
+  const uint32_t *lw[P];
+  uint8_t *sb[P];
+  uint32_t *sw[P];
+  uint32_t sh[P], dsh[P], lo[P], carry[P], vfirst[P], vlast[P];
+  int d[P], tmax[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int li = li0 + p;
+    const int a0 = imis + (l0 + li) * Sl;
+    const int b = a0 + L;  // this line's EOL
+    const uint32_t x = __funnelshift_r(win[b >> 2], win[(b >> 2) + 1], 8 * (b & 3));
+    if ((x & eolm) != eolw) bad |= 0x80u;
+    lw[p] = win + (a0 >> 2);
+    sh[p] = 8u * static_cast<uint32_t>(a0);  // funnel shift, mod 32
+    const int o = om + 3 * G * li;             // stream byte i -> slice[o + i]
+    d[p] = (-o) & 3;                           // bytes before the first aligned word
+    dsh[p] = 8u * static_cast<uint32_t>(d[p]);
+    sb[p] = slice + o;
+    sw[p] = reinterpret_cast<uint32_t *>(sb[p] + d[p]);  // aligned word t -> sw[t]
+    tmax[p] = ((3 * G - d[p]) >> 2) - 1;                  // last aligned word inside the stream
+    lo[p] = lw[p][0];
+    carry[p] = 0;
+    vfirst[p] = vlast[p] = 0;
+  }
+  auto quad = [&](int p, uint32_t hi) -> uint32_t {
+    const uint32_t w = __funnelshift_r(lo[p], hi, sh[p]);
+    lo[p] = hi;
+    const uint32_t v0 = lds_u8((w & 0xFFu) | tb);
+    const uint32_t v1 = lds_u8(__byte_perm(w, tb, 0x7651));
+    const uint32_t v2 = lds_u8(__byte_perm(w, tb, 0x7652));
+    const uint32_t v3 = lds_u8(__byte_perm(w, tb, 0x7653));
+    bad |= v0 | v1 | v2 | v3;
+    return ((v0 * 64u + v1) * 64u + v2) * 64u + v3;
+  };
+  // 4 quads (V0..V3: 24-bit, big-endian bytes) -> stream words S0 = b0 b1 b2
+  // b3 ... (little-endian); aligned word t = bytes d + 4t .. of the stream
+  auto emit = [&](int p, uint32_t V0, uint32_t V1, uint32_t V2, uint32_t V3, int t, int tm) {
+    const uint32_t S0 = __byte_perm(V0, V1, 0x6012);
+    const uint32_t S1 = __byte_perm(V1, V2, 0x5601);
+    const uint32_t S2 = __byte_perm(V2, V3, 0x4560);
+    if (t >= 0 && t <= tm) sw[p][t] = __funnelshift_r(carry[p], S0, dsh[p]);
+    if (t + 1 <= tm) sw[p][t + 1] = __funnelshift_r(S0, S1, dsh[p]);
+    if (t + 2 <= tm) sw[p][t + 2] = __funnelshift_r(S1, S2, dsh[p]);
+    carry[p] = S2;
+  };
+  int c = 0, t = -1;
+  for (; c + 4 <= G; c += 4, t += 3) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint32_t V0 = quad(p, lw[p][c + 1]);
+      const uint32_t V1 = quad(p, lw[p][c + 2]);
+      const uint32_t V2 = quad(p, lw[p][c + 3]);
+      const uint32_t V3 = quad(p, lw[p][c + 4]);
+      if (c == 0) vfirst[p] = V0;
+      vlast[p] = V3;
+      emit(p, V0, V1, V2, V3, t, 0x7fffffff);  // whole groups: every word inside
+    }
+  }
+  const int r = G - c;  // the remaining 0-3 quads, then the words up to tmax
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    uint32_t V0 = 0, V1 = 0, V2 = 0;
+    if (r > 0) V0 = quad(p, lw[p][c + 1]);
+    if (r > 1) V1 = quad(p, lw[p][c + 2]);
+    if (r > 2) V2 = quad(p, lw[p][c + 3]);
+    if (c == 0) vfirst[p] = V0;
+    if (r > 0) vlast[p] = r == 1 ? V0 : (r == 2 ? V1 : V2);
+    emit(p, V0, V1, V2, 0u, t, tmax[p]);
+    // head bytes [0, d) from the first quad, tail [T, 3G) from the last
+    const int T = d[p] + 4 * (tmax[p] + 1);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (i < d[p]) sb[p][i] = static_cast<uint8_t>(vfirst[p] >> (16 - 8 * i));
+      if (3 * G - 3 + i >= T) sb[p][3 * G - 3 + i] = static_cast<uint8_t>(vlast[p] >> (16 - 8 * i));
+    }
+  }
 }
 
 // DS = false: the verified line-structured fast path of b64_decode_ws.
@@ -167,6 +276,12 @@ __global__ void __launch_bounds__(kWlThreads, 1)
       // a multiple of 4 lines: 3 * (first quad of a tile) is then a multiple
       // of 4, so DIRECT stores stay 4-byte aligned in every tile
       if (kWlDirect) Lt = Lt < 4 ? 4 : Lt & ~3;
+      // line-major tiles: a whole number of blocks per compute warp when
+      // the tile holds at least one block per warp (load balance)
+      if (!DS && kWlLineMajor && G <= kWlLmMaxG) {
+        const int unit = kWlWarps * 32 * lm_stride(G, e);
+        if (Lt >= unit) Lt -= Lt % unit;
+      }
     }
     const int64_t ntiles = (nlines + Lt - 1) / Lt;
     const int64_t Q = Mc / 4;                             // complete quads
@@ -206,6 +321,24 @@ __global__ void __launch_bounds__(kWlThreads, 1)
       const int dl32 = 32 / G, dc32 = 32 % G;
       const int pstep = dl32 * Sl + 4 * dc32;
       uint8_t *slice = S.out[warp];
+      // n staged bytes at src8 (congruent to gdst mod 16) -> 16-byte stores
+      // of the aligned interior + byte stores for the edges (whole warp)
+      auto copy_out = [lane](uint8_t *gdst, const uint8_t *src8, int n) {
+        const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
+        const uintptr_t ga = (g + 15) & ~static_cast<uintptr_t>(15);
+        const uintptr_t gb = (g + static_cast<uintptr_t>(n)) & ~static_cast<uintptr_t>(15);
+        if (gb > ga) {
+          const int head = static_cast<int>(ga - g), ng = static_cast<int>((gb - ga) >> 4);
+          uint32_t sa = ptx::smem_u32(src8 + head) + 16u * lane;
+          uint4 *gp = reinterpret_cast<uint4 *>(gdst + head) + lane;  // (global: derived from out)
+          for (int i = lane; i < ng; i += 32, sa += 512u, gp += 32) *gp = ptx::lds128_a(sa);
+          const int tail0 = static_cast<int>(gb - g);
+          if (lane < head) gdst[lane] = src8[lane];
+          if (lane >= 16 && lane - 16 < n - tail0) gdst[tail0 + lane - 16] = src8[tail0 + lane - 16];
+        } else {
+          for (int i = lane; i < n; i += 32) gdst[i] = src8[i];
+        }
+      };
       // DIRECT packing: word j (lane j < 24) of a 96-byte run holds output
       // bytes 4j..4j+3 = bytes r.. of lane ps's 3 and the rest of lane ps+1's
       const int ps = lane < 24 ? (4 * lane) / 3 : 0, pr = 4 * lane - 3 * ps;
@@ -237,7 +370,10 @@ __global__ void __launch_bounds__(kWlThreads, 1)
           uint8_t *ob = slice + omis - 3 * qa;  // quad q -> ob + 3q
           uint32_t bad = 0;
           const bool interior = q1 < Q && (line0 + Lt) * static_cast<int64_t>(Sl) <= M;
-          const bool direct = !DS && kWlDirect && interior && ((reinterpret_cast<uintptr_t>(gdst) & 3) == 0);
+          // line-major (interior tiles, short lines): lane = line, below
+          const bool lmaj = !DS && kWlLineMajor && interior && G <= kWlLmMaxG;
+          const bool direct = !DS && !lmaj && kWlDirect && interior &&
+                              ((reinterpret_cast<uintptr_t>(gdst) & 3) == 0);
           if constexpr (DS) {
             // despace: each lane copies quads q = qa + lane + 32 i (the EOL
             // of every line is checked below); 4-byte aligned destination:
@@ -270,7 +406,40 @@ __global__ void __launch_bounds__(kWlThreads, 1)
               }
             }
           }
-          if constexpr (!DS) {
+          if (lmaj) {
+            // LINE-MAJOR: warp w takes 32-line blocks w, w + 16, ... of the
+            // tile, lane l line 32 b + l.  A lane's quads are consecutive in
+            // shared memory (each window word is loaded once, one funnel
+            // shift per quad with a per-line shift) and its 3G output bytes
+            // are consecutive in the warp's staging slice: every 4 quads
+            // give 3 stream words, stored as 3 aligned STS.32 (funnel-shifted
+            // by the lane's staging misalignment); the at most 3 bytes before
+            // the first / after the last aligned word are byte stores from
+            // the first / last quad.  Then the block's 96 G bytes go out as
+            // 16-byte stores (copy_out).  No per-quad line bookkeeping.
+            const int strd = lm_stride(G, e);
+            const int BL = 32 * strd;  // lines per block
+            const int nblk = (Lt + BL - 1) >> (strd == 2 ? 6 : 5);
+            for (int blk = warp; blk < nblk; blk += kWlWarps) {
+              const int l0 = blk * BL;
+              const int nl = Lt - l0 < BL ? Lt - l0 : BL;
+              uint8_t *gb = out + 3 * (q0 + static_cast<int64_t>(l0) * G);
+              const int om = static_cast<int>(reinterpret_cast<uintptr_t>(gb) & 15);
+              __syncwarp();  // the previous block's copy-out has read the slice
+              if (strd == 2 && nl == 64) {
+                // full 64-line block: the lane's two lines interleaved (ILP)
+                lm_lines<2>(win, slice, imis, Sl, L, G, om, l0, 2 * lane, tb, eolw, eolm, bad);
+              } else {
+                for (int pass = 0; pass < strd; ++pass) {
+                  const int li = strd * lane + pass;  // this lane's line in the block
+                  if (li < nl) lm_lines<1>(win, slice, imis, Sl, L, G, om, l0, li, tb, eolw, eolm, bad);
+                }
+              }
+              __syncwarp();
+              copy_out(gb, slice + om, 3 * G * nl);
+            }
+          }
+          if constexpr (!DS) if (!lmaj) {
           // DIRECT (B64_WL_DIRECT, 4-byte aligned output): interior warps pack
           // 32 lanes' 3-byte results into 24 words with two shuffles and write
           // them with one coalesced 4-byte store per lane -- no staging slice,
@@ -435,6 +604,7 @@ __global__ void __launch_bounds__(kWlThreads, 1)
           }
           }  // !DS
           // EOL of every line whose last quad this warp owns (and that has one)
+          if (!lmaj)
           for (int ln = line_of(qa) + lane, lb = line_of(qb); ln < lb; ln += 32) {
             if ((line0 + ln + 1) * Sl > M) break;
             const int b = imis + ln * Sl + L;
@@ -446,25 +616,10 @@ __global__ void __launch_bounds__(kWlThreads, 1)
               S.flag = 1;
               atomicExch(&st->viol, 1);
             }
-          } else if (!DS && qa < qb && !direct) {
+          } else if (!DS && !lmaj && qa < qb && !direct) {
             // this warp's bytes: congruent staging -> 16-byte stores + byte edges
             __syncwarp();
-            const int n = 3 * (qb - qa);
-            const uint8_t *src8 = slice + omis;
-            const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
-            const uintptr_t ga = (g + 15) & ~static_cast<uintptr_t>(15);
-            const uintptr_t gb = (g + static_cast<uintptr_t>(n)) & ~static_cast<uintptr_t>(15);
-            if (gb > ga) {
-              const int head = static_cast<int>(ga - g), ng = static_cast<int>((gb - ga) >> 4);
-              for (int i = lane; i < ng; i += 32)
-                *reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(ga) + 16 * i) =
-                    ptx::lds128(src8 + head + 16 * i);
-              const int tail0 = static_cast<int>(gb - g);
-              if (lane < head) gdst[lane] = src8[lane];
-              if (lane >= 16 && lane - 16 < n - tail0) gdst[tail0 + lane - 16] = src8[tail0 + lane - 16];
-            } else {
-              for (int i = lane; i < n; i += 32) gdst[i] = src8[i];
-            }
+            copy_out(gdst, slice + omis, 3 * (qb - qa));
           }
         }
         __syncwarp();

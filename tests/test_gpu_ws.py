@@ -185,12 +185,18 @@ def test_fast_path_taken_exactly_on_line_structure():
     check(u)
 
 
-@pytest.mark.parametrize("L", [4, 8, 60, 64, 76, 1000, 4092])
+# L: G = L / 4 quads per line; the interior tiles take the line-major path
+# for G <= 32 (one lane per line, lane stride 1 or 2 by (G, e)), the flat
+# path above; 24 / 40 / 68: stride-2 maps, 60: stride 2 with CR LF and 1
+# with LF, 80 / 128: stride 1, 132: flat
+@pytest.mark.parametrize("L", [4, 8, 24, 40, 60, 64, 68, 76, 80, 128, 132, 1000, 4092])
 @pytest.mark.parametrize("crlf", [False, True])
 def test_line_structured_lengths(L, crlf):
     # the fast path across tile seams for every line length; tails of 1..L chars
-    x = splitmix_bytes(421 + L, 0, 300_000)
-    for n in [1, 2, 3, 3 * L // 4, 3 * L // 4 + 1, 7 * L, 300_000]:
+    x = splitmix_bytes(421 + L, 0, 600_000)
+    for n in [1, 2, 3, 3 * L // 4, 3 * L // 4 + 1, 7 * L, 300_000, 600_000 - 1]:
         w = oracle.encode_wrapped(x[:n], L, crlf=crlf)
         check(w)
         check(w[: w.size - (2 if crlf else 1)])  # without the final EOL
+        if n >= 300_000:
+            assert _verdict(w) == 1

@@ -38,6 +38,14 @@ VARIANTS = {
     "b_p7": {"B64_BATCH_PASSES": 7},
     "sw20": {"B64_WARPS_C": 20},
     "wlw24": {"B64_WL_WARPS": 24},
+    "wlw20": {"B64_WL_WARPS": 20},
+    "wlw24t64": {"B64_WL_WARPS": 24, "B64_WL_TILE": 65536},
+    "wlw16t64": {"B64_WL_TILE": 65536},
+    "wlw20t64": {"B64_WL_WARPS": 20, "B64_WL_TILE": 65536},
+    "wl_nolm": {"B64_WL_LINEMAJOR": 0},
+    "wlt78": {"B64_WL_TILE": 79872},
+    "wlt80": {"B64_WL_TILE": 81920},
+    "wlt78_nolm": {"B64_WL_TILE": 79872, "B64_WL_LINEMAJOR": 0},
     "wlw30": {"B64_WL_WARPS": 30},
     "wlw12": {"B64_WL_WARPS": 12},
     "sw12": {"B64_WARPS_C": 12},
