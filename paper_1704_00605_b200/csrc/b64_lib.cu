@@ -29,6 +29,7 @@
 #include "b64_ws.cuh"
 #include "b64_wrap.cuh"
 #include "b64_wslines.cuh"
+#include "b64_wraplines.cuh"
 
 // f3 / f4 general path: the two-pass mask + compaction kernels
 // (b64_compact.cuh, b64_ws.cuh).  B64_CP_ONEPASS=1 (measurement only, see
@@ -512,6 +513,8 @@ DevInfo *device_setup_info(int *dev_out) {
     if (set_smem(encode_wrap_kernel<2, true>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
     if (set_smem(encode_wrap_kernel<2, false>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
     if (set_smem(encode_wrap_kernel<1, false>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(encode_lines_kernel<1>, sizeof(ElSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(encode_lines_kernel<2>, sizeof(ElSmem)) != cudaSuccess) return nullptr;
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
 #if B64_CP_ONEPASS
     if (set_smem(despace1_kernel, sizeof(OpDsSmem)) != cudaSuccess) return nullptr;
@@ -1196,6 +1199,31 @@ int64_t b64_encode_wrapped(const uint8_t *d_in, int64_t n, uint8_t *d_out, int l
   W.G = line_chars / 4;
   W.nlines = (W.m + W.L - 1) / W.L;
   W.total = W.m + W.e * W.nlines;
+  if (B64_WR_LINEMAJOR && W.G <= kElMaxG) {
+    // line-major kernel (b64_wraplines.cuh): tiles of whole lines, a whole
+    // number of 32 / 64-line blocks per compute warp where the tile allows
+    ElGeom E;
+    E.n = n;
+    E.m = W.m;
+    E.nlines = W.nlines;
+    E.nfull = n / (3 * W.G);
+    E.L = W.L;
+    E.e = W.e;
+    E.G = W.G;
+    E.strd = lm_stride(W.G, W.e);
+    int Lt = kElIn / (3 * W.G);
+    const int unit = kElWarps * 32 * E.strd;
+    if (Lt >= unit) Lt -= Lt % unit;
+    const int64_t want = (W.nlines + 2 * static_cast<int64_t>(sms) - 1) / (2 * static_cast<int64_t>(sms));
+    if (want < Lt) Lt = want < 1 ? 1 : static_cast<int>(want);
+    E.Lt = Lt;
+    E.ntiles = (W.nlines + Lt - 1) / Lt;
+    const int64_t grid = E.ntiles < sms ? E.ntiles : sms;
+    auto f = crlf ? encode_lines_kernel<2> : encode_lines_kernel<1>;
+    f<<<static_cast<unsigned>(grid), kElThreads, sizeof(ElSmem), stream>>>(d_in, d_out, E, flags);
+    if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
+    return W.total;
+  }
   W.Lt = kWrIn / (3 * W.G);
   if (W.Lt > B64_WR_OUT / (W.L + W.e)) W.Lt = B64_WR_OUT / (W.L + W.e);
   W.inv = W.G > 1 ? static_cast<uint32_t>(((1ull << 32) + W.G - 1) / W.G) : 0u;

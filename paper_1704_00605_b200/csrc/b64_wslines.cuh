@@ -59,7 +59,7 @@ constexpr int kWlLmMaxG = 32;  // quads per line up to which the line-major path
 // 2(L + e) bytes apart) -- from a bank simulation of both maps, bit
 // G - 1 + 32 (e - 1) set = stride 2 (G <= 19: 64 lines of staging fit).
 constexpr uint64_t kWlLmStride2 = 0x77f7800072620ull;
-__device__ __forceinline__ int lm_stride(int G, int e) {
+__host__ __device__ __forceinline__ int lm_stride(int G, int e) {
   return ((kWlLmStride2 >> (G - 1 + 32 * (e - 1))) & 1) ? 2 : 1;
 }
 #ifndef B64_WL_STAGES
