@@ -51,6 +51,9 @@ constexpr bool kWlDirect = B64_WL_DIRECT != 0;
 #define B64_WL_LINEMAJOR 1
 #endif
 constexpr bool kWlLineMajor = B64_WL_LINEMAJOR != 0;
+#ifndef B64_WL_BULK  // line-major blocks: one bulk (TMA) store per block by lane 0
+#define B64_WL_BULK 1
+#endif
 constexpr int kWlLmMaxG = 32;  // quads per line up to which the line-major path runs
 // Line-major lane -> line map: stride 1 (lane l: line l of a 32-line block)
 // or 2 (lane l: lines 2l and 2l + 1 of a 64-line block, two passes), per
@@ -343,6 +346,36 @@ __global__ void __launch_bounds__(kWlThreads, 1)
       // bytes 4j..4j+3 = bytes r.. of lane ps's 3 and the rest of lane ps+1's
       const int ps = lane < 24 ? (4 * lane) / 3 : 0, pr = 4 * lane - 3 * ps;
       const uint32_t psel = pr == 0 ? 0x4210u : (pr == 1 ? 0x5421u : 0x6542u);
+#if B64_WL_BULK
+      // line-major blocks leave as one bulk (TMA) store of their aligned
+      // interior by lane 0 (edges byte-wise); the slice is restaged only
+      // after that store has read it
+      const uint64_t opol = ptx::policy_evict_first();
+      bool bulk_pending = false;
+      auto bulk_wait_slice = [&]() {
+        if (bulk_pending) {
+          if (lane == 0) ptx::bulk_wait_read<0>();
+          bulk_pending = false;
+        }
+      };
+      auto bulk_out = [&](uint8_t *gd, const uint8_t *src8, int n) {
+        const uintptr_t g = reinterpret_cast<uintptr_t>(gd);
+        const uintptr_t ga = (g + 15) & ~static_cast<uintptr_t>(15);
+        const uintptr_t ge = (g + static_cast<uintptr_t>(n)) & ~static_cast<uintptr_t>(15);
+        if (ge > ga) {
+          const int head = static_cast<int>(ga - g), tail0 = static_cast<int>(ge - g);
+          if (lane == 0) {
+            ptx::bulk_s2g(gd + head, src8 + head, static_cast<uint32_t>(ge - ga), opol);
+            ptx::bulk_commit();
+          }
+          if (lane < head) gd[lane] = src8[lane];
+          if (lane >= 16 && lane - 16 < n - tail0) gd[tail0 + lane - 16] = src8[tail0 + lane - 16];
+          bulk_pending = true;
+        } else {
+          for (int i = lane; i < n; i += 32) gd[i] = src8[i];
+        }
+      };
+#endif
       int k = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
         const int s = k % kWlStages;
@@ -425,6 +458,9 @@ __global__ void __launch_bounds__(kWlThreads, 1)
               const int nl = Lt - l0 < BL ? Lt - l0 : BL;
               uint8_t *gb = out + 3 * (q0 + static_cast<int64_t>(l0) * G);
               const int om = static_cast<int>(reinterpret_cast<uintptr_t>(gb) & 15);
+#if B64_WL_BULK
+              bulk_wait_slice();
+#endif
               __syncwarp();  // the previous block's copy-out has read the slice
               if (strd == 2 && nl == 64) {
                 // full 64-line block: the lane's two lines interleaved (ILP)
@@ -435,10 +471,22 @@ __global__ void __launch_bounds__(kWlThreads, 1)
                   if (li < nl) lm_lines<1>(win, slice, imis, Sl, L, G, om, l0, li, tb, eolw, eolm, bad);
                 }
               }
+#if B64_WL_BULK
+              ptx::fence_proxy_async_smem();  // this lane's staging stores vs the bulk store
+              __syncwarp();
+              bulk_out(gb, slice + om, 3 * G * nl);
+#else
               __syncwarp();
               copy_out(gb, slice + om, 3 * G * nl);
+#endif
             }
           }
+#if B64_WL_BULK
+          if (!lmaj) {
+            bulk_wait_slice();  // a staged path below may restage the slice
+            __syncwarp();
+          }
+#endif
           if constexpr (!DS) if (!lmaj) {
           // DIRECT (B64_WL_DIRECT, 4-byte aligned output): interior warps pack
           // 32 lanes' 3-byte results into 24 words with two shuffles and write
@@ -625,6 +673,9 @@ __global__ void __launch_bounds__(kWlThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&S.empty[s]);
       }
+#if B64_WL_BULK
+      if (lane == 0) ptx::bulk_wait<0>();
+#endif
     }
     viol = S.flag != 0;
   }

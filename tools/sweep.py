@@ -44,6 +44,7 @@ VARIANTS = {
     "wlw20t64": {"B64_WL_WARPS": 20, "B64_WL_TILE": 65536},
     "wl_nolm": {"B64_WL_LINEMAJOR": 0},
     "el_bulk0": {"B64_EL_BULK": 0},
+    "wl_bulk0": {"B64_WL_BULK": 0},
     "el_off": {"B64_WR_LINEMAJOR": 0},
     "wlt78": {"B64_WL_TILE": 79872},
     "wlt80": {"B64_WL_TILE": 81920},
