@@ -193,6 +193,57 @@ __device__ __forceinline__ void lm_lines(const uint32_t *win, uint8_t *slice, in
   }
 }
 
+// Despace line-major: line li of a block (first line l0 of the tile) -- its
+// L = 4G characters go to slice[om + 4G li ..) word by word (funnel-shifted
+// from the window, and to the slice's alignment when om is not a multiple
+// of 4), each word checked for a byte < 0x21 (white space or a control
+// byte inside a line: not line-structured); the EOL is checked too.
+__device__ __forceinline__ void ds_line(const uint32_t *win, uint8_t *slice, int imis, int Sl, int L,
+                                        int G, int om, int l0, int li, uint32_t eolw, uint32_t eolm,
+                                        uint32_t &bad) {
+  const int a0 = imis + (l0 + li) * Sl;
+  {
+    const int b = a0 + L;
+    const uint32_t x = __funnelshift_r(win[b >> 2], win[(b >> 2) + 1], 8 * (b & 3));
+    if ((x & eolm) != eolw) bad |= 0x80u;
+  }
+  const uint32_t *lw = win + (a0 >> 2);
+  const uint32_t sh = 8u * static_cast<uint32_t>(a0);
+  const int o = om + 4 * G * li;
+  const int d = (-o) & 3;  // the same for every line of the block (4G = 0 mod 4)
+  uint8_t *sb = slice + o;
+  uint32_t *sw = reinterpret_cast<uint32_t *>(sb + d);
+  uint32_t lo = lw[0], chk = 0;
+  if (d == 0) {
+#pragma unroll 4
+    for (int j = 0; j < G; ++j) {
+      const uint32_t hi = lw[j + 1];
+      const uint32_t w = __funnelshift_r(lo, hi, sh);
+      lo = hi;
+      chk |= (w - 0x21212121u) & ~w;  // has_below_0x21, OR-ed over the line
+      sw[j] = w;
+    }
+  } else {
+    const uint32_t dsh = 8u * static_cast<uint32_t>(d);
+    uint32_t prev = __funnelshift_r(lo, lw[1], sh), first = prev;
+    lo = lw[1];
+    chk |= (prev - 0x21212121u) & ~prev;
+#pragma unroll 4
+    for (int j = 1; j < G; ++j) {
+      const uint32_t hi = lw[j + 1];
+      const uint32_t w = __funnelshift_r(lo, hi, sh);
+      lo = hi;
+      chk |= (w - 0x21212121u) & ~w;
+      sw[j - 1] = __funnelshift_r(prev, w, dsh);
+      prev = w;
+    }
+    // head bytes [0, d) of the first word, tail: the last 4 - d bytes
+    for (int i = 0; i < d; ++i) sb[i] = static_cast<uint8_t>(first >> (8 * i));
+    for (int i = d; i < 4; ++i) sb[4 * G - 4 + i] = static_cast<uint8_t>(prev >> (8 * i));
+  }
+  if (chk & 0x80808080u) bad |= 0x80u;
+}
+
 // DS = false: the verified line-structured fast path of b64_decode_ws.
 // DS = true: the same for b64_despace (Appendix B on MIME / PEM text): every
 // quad of kept characters is copied to out + 4 q (a quad never straddles a
@@ -404,10 +455,39 @@ __global__ void __launch_bounds__(kWlThreads, 1)
           uint32_t bad = 0;
           const bool interior = q1 < Q && (line0 + Lt) * static_cast<int64_t>(Sl) <= M;
           // line-major (interior tiles, short lines): lane = line, below
-          const bool lmaj = !DS && kWlLineMajor && interior && G <= kWlLmMaxG;
+          // (despace: odd G only -- lanes 4G bytes apart in the staging slice
+          // are bank-conflict-free exactly when G is odd -- and 32 lines of
+          // 4G bytes must fit the slice)
+          const bool lmaj = kWlLineMajor && interior &&
+                            (DS ? ((G & 1) != 0 && 128 * G + 16 <= kWlSlice) : G <= kWlLmMaxG);
           const bool direct = !DS && !lmaj && kWlDirect && interior &&
                               ((reinterpret_cast<uintptr_t>(gdst) & 3) == 0);
-          if constexpr (DS) {
+          if constexpr (DS) if (lmaj) {
+            // despace, LINE-MAJOR: 32-line blocks, lane l line 32 b + l; its
+            // L kept characters are copied (and checked) word by word into
+            // the staging slice, the block leaves as one bulk store
+            const int nblk = (Lt + 31) >> 5;
+            for (int blk = warp; blk < nblk; blk += kWlWarps) {
+              const int l0 = blk * 32;
+              const int nl = Lt - l0 < 32 ? Lt - l0 : 32;
+              uint8_t *gb = out + 4 * (q0 + static_cast<int64_t>(l0) * G);
+              const int om = static_cast<int>(reinterpret_cast<uintptr_t>(gb) & 15);
+#if B64_WL_BULK
+              bulk_wait_slice();
+#endif
+              __syncwarp();
+              if (lane < nl) ds_line(win, slice, imis, Sl, L, G, om, l0, lane, eolw, eolm, bad);
+#if B64_WL_BULK
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              bulk_out(gb, slice + om, 4 * G * nl);
+#else
+              __syncwarp();
+              copy_out(gb, slice + om, 4 * G * nl);
+#endif
+            }
+          }
+          if constexpr (DS) if (!lmaj) {
             // despace: each lane copies quads q = qa + lane + 32 i (the EOL
             // of every line is checked below); 4-byte aligned destination:
             // one coalesced STG.32 per quad, else byte stores
@@ -439,7 +519,7 @@ __global__ void __launch_bounds__(kWlThreads, 1)
               }
             }
           }
-          if (lmaj) {
+          if constexpr (!DS) if (lmaj) {
             // LINE-MAJOR: warp w takes 32-line blocks w, w + 16, ... of the
             // tile, lane l line 32 b + l.  A lane's quads are consecutive in
             // shared memory (each window word is loaded once, one funnel
