@@ -501,13 +501,13 @@ DevInfo *device_setup_info(int *dev_out) {
     if (set_smem(despace_kernel, sizeof(DsSmem)) != cudaSuccess) return nullptr;
     if (set_smem(decode_ws_kernel, sizeof(WsSmem)) != cudaSuccess) return nullptr;
     if (set_smem(decode_lines_kernel<false>, sizeof(WlSmem)) != cudaSuccess) return nullptr;
-    if (set_smem(decode_lines_kernel<true>, sizeof(WlSmem)) != cudaSuccess) return nullptr;
+    if (set_smem(decode_lines_kernel<true>, sizeof(WlSmemT<true>)) != cudaSuccess) return nullptr;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.wl_ctas, decode_lines_kernel<false>,
                                                       kWlThreads, sizeof(WlSmem)) != cudaSuccess ||
         di.wl_ctas < 1)
       di.wl_ctas = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.dl_ctas, decode_lines_kernel<true>,
-                                                      kWlThreads, sizeof(WlSmem)) != cudaSuccess ||
+                                                      kWlThreads, sizeof(WlSmemT<true>)) != cudaSuccess ||
         di.dl_ctas < 1)
       di.dl_ctas = 1;
     if (set_smem(encode_wrap_kernel<2, true>, sizeof(WrSmem)) != cudaSuccess) return nullptr;
@@ -1080,7 +1080,7 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
   // copy with the line structure checked; 2-3. the general two-pass path,
   // whose kernels return at once when 1. succeeded.
   if (cudaMemsetAsync(wl, 0, sizeof(WlState), stream) != cudaSuccess) return B64_ERR_CUDA;
-  decode_lines_kernel<true><<<static_cast<unsigned>(di->sms * di->dl_ctas), kWlThreads, sizeof(WlSmem),
+  decode_lines_kernel<true><<<static_cast<unsigned>(di->sms * di->dl_ctas), kWlThreads, sizeof(WlSmemT<true>),
                               stream>>>(d_in, m, d_out, wl, nullptr, 0, d_out_len);
   cp_mask_kernel<<<static_cast<unsigned>(grid), kCpThreads, 0, stream>>>(d_in, m, tpc, counts,
                                                                           masks, nullptr, &wl->verdict);

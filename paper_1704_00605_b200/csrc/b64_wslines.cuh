@@ -86,15 +86,33 @@ struct WlState {
   int32_t pad;
 };
 
-struct alignas(128) WlSmem {
-  uint8_t in[kWlStages][kWlTile + 64];
-  alignas(16) uint8_t out[kWlWarps][kWlSlice];
-  uint64_t full[kWlStages];
-  uint64_t empty[kWlStages];
+// Despace (DS) ring: its line-major copy is cheap enough that the input
+// pipeline depth decides, so it takes more, smaller stages than the decode
+#ifndef B64_DS_TILE
+#define B64_DS_TILE 49920
+#endif
+#ifndef B64_DS_STAGES
+#define B64_DS_STAGES 3
+#endif
+template <bool DS>
+struct WlCfg {
+  static constexpr int kTile = DS ? B64_DS_TILE : kWlTile;
+  static constexpr int kStages = DS ? B64_DS_STAGES : kWlStages;
+  static constexpr int kWarpQuads = ((kTile / 4 + kWlWarps - 1) / kWlWarps + 31) / 32 * 32;
+  static constexpr int kSlice = 3 * kWarpQuads + 48 > 3696 ? 3 * kWarpQuads + 48 : 3696;
+};
+
+template <bool DS>
+struct alignas(128) WlSmemT {
+  uint8_t in[WlCfg<DS>::kStages][WlCfg<DS>::kTile + 64];
+  alignas(16) uint8_t out[kWlWarps][WlCfg<DS>::kSlice];
+  uint64_t full[WlCfg<DS>::kStages];
+  uint64_t empty[WlCfg<DS>::kStages];
   int64_t geo[4];   // Mc (kept chars), nlines, ok
   int32_t Le[2];    // L, e
   int32_t flag;
 };
+using WlSmem = WlSmemT<false>;
 
 // Any byte of w below 0x21 (' ', '\n', '\r' and the other control bytes):
 // the classic "has less than" SWAR test, exact as an any-test for bytes
@@ -257,11 +275,12 @@ __global__ void __launch_bounds__(kWlThreads, 1)
     decode_lines_kernel(const uint8_t *__restrict__ in, int64_t M, uint8_t *__restrict__ out,
                         WlState *st, b64_result *res, int flags, int64_t *ds_out_len) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  WlSmem &S = *reinterpret_cast<WlSmem *>(smem_raw);
+  using C = WlCfg<DS>;
+  WlSmemT<DS> &S = *reinterpret_cast<WlSmemT<DS> *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < 256) g_dec_tab[tid] = kInvalid;
   if (tid == 0) {
-    for (int s = 0; s < kWlStages; ++s) {
+    for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&S.full[s], 1);
       ptx::mbar_init(&S.empty[s], kWlWarps);
     }
@@ -323,7 +342,7 @@ __global__ void __launch_bounds__(kWlThreads, 1)
     // lines per tile: as many as fit (large tiles amortise the per-tile
     // work -- 28 KiB: 0.616 ms, 76 KiB: 0.529 ms on the mime workload), but
     // at least two tiles per CTA for small inputs
-    int Lt = kWlTile / Sl;
+    int Lt = C::kTile / Sl;
     {
       const int64_t want = (nlines + 2 * static_cast<int64_t>(gridDim.x) - 1) / (2 * static_cast<int64_t>(gridDim.x));
       if (want < Lt) Lt = want < 1 ? 1 : static_cast<int>(want);
@@ -350,12 +369,12 @@ __global__ void __launch_bounds__(kWlThreads, 1)
         const uint64_t pol = ptx::policy_evict_first();
         int k = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-          const int s = k % kWlStages;
-          if (k >= kWlStages) {
+          const int s = k % C::kStages;
+          if (k >= C::kStages) {
             if (B64_WL_SLEEP > 0)
-              ptx::mbar_wait_sleep(&S.empty[s], static_cast<uint32_t>((k / kWlStages - 1) & 1), B64_WL_SLEEP);
+              ptx::mbar_wait_sleep(&S.empty[s], static_cast<uint32_t>((k / C::kStages - 1) & 1), B64_WL_SLEEP);
             else
-              ptx::mbar_wait(&S.empty[s], static_cast<uint32_t>((k / kWlStages - 1) & 1));
+              ptx::mbar_wait(&S.empty[s], static_cast<uint32_t>((k / C::kStages - 1) & 1));
           }
           const int64_t src = t * Lt * static_cast<int64_t>(Sl);
           const int64_t tl = static_cast<int64_t>(Lt) * Sl;
@@ -429,8 +448,8 @@ __global__ void __launch_bounds__(kWlThreads, 1)
 #endif
       int k = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-        const int s = k % kWlStages;
-        ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((k / kWlStages) & 1));
+        const int s = k % C::kStages;
+        ptx::mbar_wait_spin(&S.full[s], static_cast<uint32_t>((k / C::kStages) & 1));
         int stop = 0;
         // another CTA's violation only needs to stop this one eventually (the
         // verdict is decided at the end): poll the global flag every 8th tile
@@ -459,7 +478,7 @@ __global__ void __launch_bounds__(kWlThreads, 1)
           // are bank-conflict-free exactly when G is odd -- and 32 lines of
           // 4G bytes must fit the slice)
           const bool lmaj = kWlLineMajor && interior &&
-                            (DS ? ((G & 1) != 0 && 128 * G + 16 <= kWlSlice) : G <= kWlLmMaxG);
+                            (DS ? ((G & 1) != 0 && 128 * G + 16 <= C::kSlice) : G <= kWlLmMaxG);
           const bool direct = !DS && !lmaj && kWlDirect && interior &&
                               ((reinterpret_cast<uintptr_t>(gdst) & 3) == 0);
           if constexpr (DS) if (lmaj) {

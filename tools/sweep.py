@@ -45,6 +45,15 @@ VARIANTS = {
     "wl_nolm": {"B64_WL_LINEMAJOR": 0},
     "el_bulk0": {"B64_EL_BULK": 0},
     "wl_bulk0": {"B64_WL_BULK": 0},
+    "ds_s2_t78": {"B64_DS_STAGES": 2, "B64_DS_TILE": 79872},
+    "ds_s3_t39": {"B64_DS_TILE": 39936},
+    "ds_s3_t45": {"B64_DS_TILE": 44928},
+    "ds_s3_t56": {"B64_DS_TILE": 56160},
+    "ds_s4_t39": {"B64_DS_STAGES": 4, "B64_DS_TILE": 39936},
+    "ds_s4_t42": {"B64_DS_STAGES": 4, "B64_DS_TILE": 42120},
+    "wl_s3_t52": {"B64_WL_STAGES": 3, "B64_WL_TILE": 53248},
+    "wl_s3_t48": {"B64_WL_STAGES": 3, "B64_WL_TILE": 49920},
+    "wl_s4_t39": {"B64_WL_STAGES": 4, "B64_WL_TILE": 39936},
     "el_off": {"B64_WR_LINEMAJOR": 0},
     "wlt78": {"B64_WL_TILE": 79872},
     "wlt80": {"B64_WL_TILE": 81920},
