@@ -265,8 +265,8 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
  * 64 = PEM).  The paper's comparison mentions MIME-style line handling in
  * the Linux codec.  d_out capacity:
  * b64_encoded_len_wrapped(n, line_chars, crlf, flags).  Asynchronous on
- * `stream`; returns the output length, or B64_ERR_ARG (nothing launched) /
- * B64_ERR_CUDA. */
+ * `stream` (one kernel: line-major for line_chars <= 128); returns the
+ * output length, or B64_ERR_ARG (nothing launched) / B64_ERR_CUDA. */
 int64_t b64_encoded_len_wrapped(int64_t n, int line_chars, int crlf, int flags);
 int64_t b64_encode_wrapped(const uint8_t *d_in, int64_t n, uint8_t *d_out, int line_chars,
                            int crlf, int flags, b64_stream_t stream);
@@ -282,7 +282,9 @@ int64_t b64_encode_wrapped(const uint8_t *d_in, int64_t n, uint8_t *d_out, int l
  * of the kept byte the decoder rejected); out_len counts decoded bytes.
  * d_out capacity: b64_decoded_max_len_ex(m, flags).  d_ws: device scratch
  * of b64_decode_ws_workspace_bytes(m) bytes, 16-byte aligned, not shared
- * with a concurrent call.  Two kernels on `stream`.
+ * with a concurrent call.  Three kernels on `stream`: a verified fast path
+ * for line-structured (MIME / PEM) text, then the mask pass and the fused
+ * compaction + decode, which return at once when the fast path succeeded.
  * _async writes the result record to d_result (device memory); the plain
  * call synchronizes `stream` and returns the status. */
 size_t b64_decode_ws_workspace_bytes(int64_t m);
