@@ -37,7 +37,7 @@ $NCU -k regex:"cp_mask|despace_kernel" -s 4 -c 2 -o gpurun_out/${T}_despaceirr -
 BM="python bench.py --workload mime --steps 1 --warmup 3"
 $BM > gpurun_out/${T}_mimeplain.json 2>&1 && \
 $NCU -k regex:"decode_lines" -s 3 -c 1 -o gpurun_out/${T}_mime -f $BM > gpurun_out/${T}_ncu_mime.log 2>&1
-$NCU -k regex:"encode_wrap" -s 3 -c 1 -o gpurun_out/${T}_mimeenc -f $BM > gpurun_out/${T}_ncu_mimeenc.log 2>&1
+$NCU -k regex:"encode_(wrap|lines)" -s 3 -c 1 -o gpurun_out/${T}_mimeenc -f $BM > gpurun_out/${T}_ncu_mimeenc.log 2>&1
 BI="python bench.py --workload mime_irregular --steps 1 --warmup 3"
 $BI > gpurun_out/${T}_mimeirrplain.json 2>&1 && \
 $NCU -k regex:"cp_mask|decode_ws" -s 6 -c 2 -o gpurun_out/${T}_mimeirr -f $BI > gpurun_out/${T}_ncu_mimeirr.log 2>&1
