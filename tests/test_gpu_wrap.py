@@ -76,3 +76,46 @@ def test_large_and_roundtrip_through_ws_decode():
     w = b64.b64_encode_wrapped(d, line_chars=76, crlf=True)
     y, st, ep = b64.b64_decode_ws(w)
     assert (st, ep) == (0, -1) and torch.equal(y, d)
+
+
+def _lm_tile_lines(n, L, crlf):
+    """Lines per tile of the line-major encoder (b64_encode_wrapped, L <= 128),
+    as the host computes them: 57 KiB of input, a whole number of 32- or
+    64-line blocks per compute warp, >= 2 tiles per SM for small inputs."""
+    G, e = L // 4, (2 if crlf else 1)
+    strd = 2 if (0x77f7800072620 >> (G - 1 + 32 * (e - 1))) & 1 else 1
+    lt = (1024 * 57) // (3 * G)
+    unit = 16 * 32 * strd
+    if lt >= unit:
+        lt -= lt % unit
+    m = 4 * ((n + 2) // 3)
+    nlines = (m + L - 1) // L
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    want = (nlines + 2 * sms - 1) // (2 * sms)
+    return max(1, want) if want < lt else lt
+
+
+@pytest.mark.parametrize("L", [4, 24, 40, 60, 64, 76, 128])
+def test_line_major_tiles_and_seams(L):
+    """The line-major encoder across its tile seams at sizes where tiles hold
+    whole blocks per warp (two lines per lane on stride-2 maps), with and
+    without a partial final line."""
+    G = L // 4
+    for crlf in (True, False):
+        n0 = 40 << 20
+        lt = _lm_tile_lines(n0, L, crlf)
+        tin = lt * 3 * G
+        k = n0 // tin
+        x = splitmix_bytes(505 + L, 0, k * tin + 3 * G + 2)
+        for n in (k * tin, k * tin - 1, k * tin + 1, k * tin + 3 * G, k * tin + 3 * G + 2):
+            check(x[:n], L, crlf)
+
+
+def test_line_major_alignments_and_flags():
+    x = splitmix_bytes(506, 0, 20 << 20)
+    for im, om in ((1, 0), (0, 3), (7, 13), (15, 15)):
+        check(x, 76, True, 0, im, om)
+        check(x, 64, False, 0, im, om)
+    for fl in (U, NP, U | NP):
+        check(x[: (20 << 20) - 1], 76, True, fl)
+        check(x[: (20 << 20) - 2], 64, False, fl, 5, 9)

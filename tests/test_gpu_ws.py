@@ -200,3 +200,15 @@ def test_line_structured_lengths(L, crlf):
         check(w[: w.size - (2 if crlf else 1)])  # without the final EOL
         if n >= 300_000:
             assert _verdict(w) == 1
+
+
+def test_line_major_large_aligned():
+    """The line-major interior path at sizes where tiles hold whole 64-line
+    blocks per warp (two lines per lane), over input / output misalignments,
+    with the fast path's verdict checked."""
+    x = splitmix_bytes(430, 0, 20 << 20)
+    for L, crlf in ((76, True), (64, False), (40, True)):
+        w = oracle.encode_wrapped(x, L, crlf=crlf)
+        assert _verdict(w) == 1
+        for im, om in ((0, 0), (1, 0), (0, 3), (7, 13), (15, 15)):
+            check(w, 0, im, om)
