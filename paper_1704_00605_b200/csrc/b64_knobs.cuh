@@ -40,6 +40,28 @@
 #define B64_CP_ONEPASS 0
 #endif
 
+// Line-major MIME kernels (round 2); 0 = the earlier paths
+// they replaced, kept for the A/B numbers DESIGN.md cites:
+//   B64_WL_LINEMAJOR  decode_lines_kernel interior tiles one lane per line
+//                     (0: flat quads across line ends; despace too)
+//   B64_WL_BULK       line-major decode / despace blocks leave as one bulk
+//                     store (0: LDS.128 -> STG.128 by the warp)
+//   B64_WR_LINEMAJOR  b64_encode_wrapped with L <= 128 on encode_lines_kernel
+//                     (0: encode_wrap_kernel for every L)
+//   B64_EL_BULK       encode_lines_kernel blocks leave as one bulk store
+#ifndef B64_WL_LINEMAJOR
+#define B64_WL_LINEMAJOR 1
+#endif
+#ifndef B64_WL_BULK
+#define B64_WL_BULK 1
+#endif
+#ifndef B64_WR_LINEMAJOR
+#define B64_WR_LINEMAJOR 1
+#endif
+#ifndef B64_EL_BULK
+#define B64_EL_BULK 1
+#endif
+
 // (defined or not; no default)
 //   B64_BATCH_TRACE      per-warp %globaltimer stamps + b64_debug_trace()
 //                        (tools/batch_trace.py); the export is not in the

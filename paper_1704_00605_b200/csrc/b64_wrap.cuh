@@ -35,9 +35,6 @@ constexpr int kWrThreads = 512;
 #ifndef B64_WR_BULK  // tile copy-out: one bulk (TMA) store by one thread instead of LDS.128 -> STG.128
 #define B64_WR_BULK 1
 #endif
-#ifndef B64_WR_LINEMAJOR  // lines of L <= 128: the line-major kernel (b64_wraplines.cuh)
-#define B64_WR_LINEMAJOR 1
-#endif
 #ifndef B64_WR_STAGES
 #define B64_WR_STAGES 2
 #endif

@@ -30,9 +30,6 @@
 
 namespace b64 {
 
-#ifndef B64_EL_BULK  // block copy-out: one bulk (TMA) store per block by lane 0
-#define B64_EL_BULK 1
-#endif
 constexpr int kElWarps = 16;                    // compute warps
 constexpr int kElThreads = kElWarps * 32 + 32;  // + one producer (TMA) warp
 constexpr int kElStages = 2;

@@ -47,13 +47,7 @@ constexpr int kWlThreads = kWlWarps * 32 + 32;    // + one producer (TMA) warp
 #define B64_WL_DIRECT 1
 #endif
 constexpr bool kWlDirect = B64_WL_DIRECT != 0;
-#ifndef B64_WL_LINEMAJOR  // interior tiles with L <= 128: one lane per line
-#define B64_WL_LINEMAJOR 1
-#endif
 constexpr bool kWlLineMajor = B64_WL_LINEMAJOR != 0;
-#ifndef B64_WL_BULK  // line-major blocks: one bulk (TMA) store per block by lane 0
-#define B64_WL_BULK 1
-#endif
 constexpr int kWlLmMaxG = 32;  // quads per line up to which the line-major path runs
 // Line-major lane -> line map: stride 1 (lane l: line l of a 32-line block)
 // or 2 (lane l: lines 2l and 2l + 1 of a 64-line block, two passes), per
