@@ -212,3 +212,7 @@ def test_line_major_large_aligned():
         assert _verdict(w) == 1
         for im, om in ((0, 0), (1, 0), (0, 3), (7, 13), (15, 15)):
             check(w, 0, im, om)
+    for fl in (U, NP, U | NP | ST):
+        w = oracle.encode_wrapped(x[: (20 << 20) - 1], 76, crlf=True, flags=fl & ~ST)
+        assert _verdict(w, fl) == 1
+        check(w, fl, 3, 5)
