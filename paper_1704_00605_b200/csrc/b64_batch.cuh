@@ -46,6 +46,8 @@ constexpr int kBWarps = B64_BATCH_WARPS;
 constexpr int kBSlots = B64_BATCH_SLOTS;
 constexpr int kBThreads = kBWarps * 32;
 constexpr int kFlagLast = 2;  // unit is the last unit of its message
+// workspace: first_msg int32[kBatchFirstMsgSlots], then first_unit int64[same]
+constexpr int kBatchFirstMsgSlots = 1024 * B64_BATCH_WARPS;
 
 template <int P>
 struct EncUnit {
@@ -386,6 +388,11 @@ __global__ void __launch_bounds__(kBThreads, B64_BATCH_CTAS)
     block_exclusive_scan2(all_u, 0, q1, q2, t3, t4, sh);
     all_u = t3;
   }
+#if B64_BATCH_UNIT_COST
+  constexpr int64_t kUnitW = static_cast<int64_t>(UIN) * B64_BATCH_UNIT_COST / 8;
+  int64_t *first_unit = reinterpret_cast<int64_t *>(first_msg + kBatchFirstMsgSlots);
+  const int64_t all_c = all_u > 0 ? kUnitW * all_u + (in_off[k] - in_off[0]) : 0;  // total cost
+#endif
   for (int64_t r0 = i_lo; r0 < i_hi; r0 += kBThreads) {
     const int64_t i = r0 + tid;
     int64_t o = c_o, u = c_u, a = c_a, b = c_b;
@@ -402,6 +409,29 @@ __global__ void __launch_bounds__(kBThreads, B64_BATCH_CTAS)
     if (i < i_hi) {
       out_off[i] = bo + po;
       unit_off[i] = bu + pu;
+#if B64_BATCH_UNIT_COST
+      // Warps get equal ranges of estimated work: a unit costs a fixed
+      // part kW (in input-byte equivalents) plus its bytes, so message i
+      // spans the cost interval [cp, cp + kW u + len), cp = kW unit_off[i]
+      // + in_off[i] - in_off[0] (no scan beyond the unit offsets).  Warp g
+      // starts at the first unit whose cost position cp + r (kW + UIN) is
+      // >= b_g = floor(C g / GW): for the g with b_g in this interval,
+      // first_msg[g] = i and first_unit[g] = unit_off[i] + min(r, u).
+      if (all_c > 0) {
+        const int64_t GWt = static_cast<int64_t>(gridDim.x) * kBWarps;
+        const int64_t a0 = bu + pu;
+        const int64_t cp = kUnitW * a0 + (a - in_off[0]);
+        const int64_t cn = cp + kUnitW * u + (b - a);
+        const int64_t g_lo = muldiv_ceil(cp, GWt, all_c);
+        const int64_t g_hi = muldiv_ceil(cn, GWt, all_c);
+        for (int64_t g = g_lo; g < g_hi; ++g) {
+          const int64_t bg = muldiv_floor(all_c, g, GWt);
+          const int64_t r = (bg - cp + kUnitW + UIN - 1) / (kUnitW + UIN);
+          first_msg[g] = static_cast<int32_t>(i);
+          first_unit[g] = a0 + (r < u ? r : u);
+        }
+      }
+#else
       // Warps whose first unit u_begin(g) = floor(U*g/GW) lies in this
       // message's units [a, a+u): g in [ceil(a*GW/U), ceil((a+u)*GW/U)).
       if (u > 0) {
@@ -411,6 +441,7 @@ __global__ void __launch_bounds__(kBThreads, B64_BATCH_CTAS)
         const int64_t g_hi = muldiv_ceil(a0 + u, GWt, all_u);
         for (int64_t g = g_lo; g < g_hi; ++g) first_msg[g] = static_cast<int32_t>(i);
       }
+#endif
       if (DECODE) {
         const int64_t len = b - a;
         if (u == 0) {  // no complete quad: decided here (NOPAD 2-3 char tails: phase 3)
@@ -445,8 +476,13 @@ __global__ void __launch_bounds__(kBThreads, B64_BATCH_CTAS)
   const int64_t U = all_u;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kBWarps + warp;
   const int64_t GW = static_cast<int64_t>(gridDim.x) * kBWarps;
+#if B64_BATCH_UNIT_COST
+  const int64_t u_begin = U > 0 ? first_unit[gw] : 0;
+  const int64_t u_end = U > 0 ? (gw + 1 < GW ? first_unit[gw + 1] : U) : 0;
+#else
   const int64_t u_begin = U > 0 ? muldiv_floor(U, gw, GW) : 0;
   const int64_t u_end = U > 0 ? muldiv_floor(U, gw + 1, GW) : 0;
+#endif
   if (u_begin < u_end) {
   const uint64_t pol = policy_evict_first();
   // Two walkers over the same unit sequence, both in registers: the issue

@@ -34,6 +34,23 @@
 #define B64_BATCH_PREFETCH 0
 #endif
 
+// Batched kernels: batch2_kernel (b64_batch2.cuh: byte-range warps, CTA-local
+// plan, first loads before the plan, per-CTA decode results) instead of
+// batch_kernel (b64_batch.cuh: global unit plan, three grid barriers).
+#ifndef B64_BATCH_V2
+#define B64_BATCH_V2 0
+#endif
+// batch_kernel: per-unit fixed cost, in eighths of a unit's input, of the
+// work estimate that splits units among warps (0: equal unit counts).
+#ifndef B64_BATCH_UNIT_COST
+#define B64_BATCH_UNIT_COST 16
+#endif
+// batch2_kernel: per-message charge of the work coordinate, in eighths of a
+// unit's input (a unit costs a fixed part plus its bytes).
+#ifndef B64_BATCH_MSG_COST
+#define B64_BATCH_MSG_COST 4
+#endif
+
 // f3 / f4 general path: the single-read kernels of b64_onepass.cuh instead
 // of the two-pass mask + compaction kernels (slower).
 #ifndef B64_CP_ONEPASS

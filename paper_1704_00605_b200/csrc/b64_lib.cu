@@ -25,6 +25,7 @@
 #include "b64_codec.cuh"
 #include "b64_ptx.cuh"
 #include "b64_batch.cuh"
+#include "b64_batch2.cuh"
 #include "b64_compact.cuh"
 #include "b64_ws.cuh"
 #include "b64_wrap.cuh"
@@ -516,6 +517,8 @@ DevInfo *device_setup_info(int *dev_out) {
     if (set_smem(encode_lines_kernel<1>, sizeof(ElSmem)) != cudaSuccess) return nullptr;
     if (set_smem(encode_lines_kernel<2>, sizeof(ElSmem)) != cudaSuccess) return nullptr;
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
+    if (set_smem(batch2_kernel<false>, kEncRingBytes) != cudaSuccess) return nullptr;
+    if (set_smem(batch2_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
 #if B64_CP_ONEPASS
     if (set_smem(despace1_kernel, sizeof(OpDsSmem)) != cudaSuccess) return nullptr;
     if (set_smem(decode_ws1_kernel, sizeof(OpWsSmem)) != cudaSuccess) return nullptr;
@@ -640,15 +643,16 @@ int decode_launch(const uint8_t *d_in, int64_t m, int final_shard, uint8_t *d_ou
 }
 
 // Batched workspace: [per-CTA totals (2 x 1024 int64) | unit_off[k+1] (int64)
-// | first_msg[kMaxBatchCtas * kBWarps] (i32)].
-constexpr int kMaxBatchCtas = 1024;
+// | first_msg[kMaxBatchCtas * kBWarps] (i32) | first_unit[same] (i64)].
+constexpr int kMaxBatchCtas = kBatchMaxCtas;
 size_t ws_layout(int64_t k, size_t *off_units, size_t *off_done) {
   size_t o = 2 * kMaxBatchCtas * sizeof(int64_t);
   *off_units = o;
   o += static_cast<size_t>(k + 1) * sizeof(int64_t);
   o = (o + 255) & ~static_cast<size_t>(255);
-  *off_done = o;  // first_msg[grid * kBWarps] (int32): each warp's first message
-  o += static_cast<size_t>(kMaxBatchCtas) * kBWarps * sizeof(int32_t);
+  *off_done = o;  // first_msg[grid * kBWarps] (int32): each warp's first message,
+  o += static_cast<size_t>(kBatchFirstMsgSlots) * sizeof(int32_t);
+  o += static_cast<size_t>(kBatchFirstMsgSlots) * sizeof(int64_t);  // then first_unit (int64)
   return (o + 255) & ~static_cast<size_t>(255);
 }
 
@@ -863,6 +867,18 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
   void *args[] = {&a_in, &a_out, &a_k, &a_in_off, &a_out_off, &a_unit, &a_blk,
                   &a_err, &a_len, &a_st, &a_done, &a_flags};
   cudaError_t e;
+#if B64_BATCH_V2
+  void *args2[] = {&a_in, &a_out, &a_k, &a_in_off, &a_out_off, &a_blk,
+                   &a_err, &a_len, &a_st, &a_flags};
+  (void)args;
+  if (direction) {
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(batch2_kernel<true>), dim3(grid),
+                                    dim3(kBThreads), args2, kDecRingBytes, stream);
+  } else {
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(batch2_kernel<false>), dim3(grid),
+                                    dim3(kBThreads), args2, kEncRingBytes, stream);
+  }
+#else
   if (direction) {
     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(batch_kernel<true>), dim3(grid),
                                     dim3(kBThreads), args, kDecRingBytes, stream);
@@ -870,6 +886,7 @@ static int batch_common(const uint8_t *d_in, const int64_t *d_in_off, int64_t k,
     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(batch_kernel<false>), dim3(grid),
                                     dim3(kBThreads), args, kEncRingBytes, stream);
   }
+#endif
   if (e != cudaSuccess) return B64_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? B64_OK : B64_ERR_CUDA;
 }

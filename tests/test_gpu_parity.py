@@ -421,6 +421,29 @@ def test_batch_all_final_quads():
     assert (st[sb] == 1).all() and (ep[sb] == 3).all()
 
 
+def test_batch_messages_spanning_many_ctas():
+    """Messages far larger than one CTA's share of the batch (their units run
+    in many CTAs' ranges, the decode result waits for all of them), next to
+    tiny and empty ones, with in_off[0] > 0; errors in the first, a middle
+    and the last unit of the large messages."""
+    lens = np.array([5, 0, 40_000_003, 3, 1, 0, 7_000_000, 2, 9_999_999, 0], dtype=np.int64)
+    raw, off = _batch_case(lens, 118, start=7)
+    text, toff = check_encode_batch(raw, off)
+    toff = toff.astype(np.int64)
+    check_decode_batch(text, toff)
+    bad = text.copy()
+    for i, frac in ((2, 0.0), (2, 0.5), (2, 0.9999999), (6, 0.999), (8, 0.3)):
+        a, b = int(toff[i]), int(toff[i + 1])
+        bad[a + int((b - a - 1) * frac)] = ord("*")
+    check_decode_batch(bad, toff)
+    # one message only: every CTA works on it, the owner finishes it
+    raw1, off1 = _batch_case(np.array([64 << 20], dtype=np.int64), 119)
+    t1, to1 = check_encode_batch(raw1, off1)
+    t1 = t1.copy()
+    t1[-5] = ord("#")
+    check_decode_batch(t1, to1.astype(np.int64))
+
+
 def test_batch_empty_and_zero_messages():
     raw, off = _batch_case(np.array([0, 0, 5, 0], dtype=np.int64), 116)
     check_encode_batch(raw, off)

@@ -41,6 +41,16 @@ for rep in range(4):
 lib.b64_debug_trace(ctypes.addressof(buf), N)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64, 4).astype(np.int64)
 nw = int(os.environ.get("B64_TRACE_WARPS", "16"))
+if os.environ.get("B64_TRACE_EXT"):  # batch2_kernel: warps 32.. hold start / searched / issued / grid-synced
+    x = a[:, 32:32 + nw, :].reshape(-1, 4)
+    t0x = x[:, 0].min()
+    for i, name in enumerate(["k_start", "searched", "issued", "gsynced"]):
+        v = (x[:, i] - t0x) / 1000.0
+        print(f"{name:10} min {v.min():7.2f} p50 {np.median(v):7.2f} max {v.max():7.2f} us")
+    y = a[:, :nw, :].reshape(-1, 4)
+    for i, name in ((1, "plan_done"), (2, "first_data"), (3, "done")):
+        v = (y[:, i] - t0x) / 1000.0
+        print(f"{name:10} min {v.min():7.2f} p50 {np.median(v):7.2f} max {v.max():7.2f} us (from kernel start)")
 a = a[:, :nw, :].reshape(-1, 4)
 if True:  # slot 0 holds (bytes << 20 | units) of the warp (trace builds)
     wb = a[:, 0] >> 20

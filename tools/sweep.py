@@ -20,6 +20,19 @@ SRC = os.path.join(ROOT, "paper_1704_00605_b200", "csrc", "b64_lib.cu")
 # Before commit "w16 c1 in3": the defaults were 8 warps x 2 CTAs/SM, 4 input stages.
 VARIANTS = {
     "base": {},
+    "batch_v1": {"B64_BATCH_V2": 0},
+    "uc0": {"B64_BATCH_UNIT_COST": 0},
+    "uc2": {"B64_BATCH_UNIT_COST": 2},
+    "uc8": {"B64_BATCH_UNIT_COST": 8},
+    "uc16": {"B64_BATCH_UNIT_COST": 16},
+    "uc4": {"B64_BATCH_UNIT_COST": 4},
+    "uc32": {"B64_BATCH_UNIT_COST": 32},
+    "batch_v2": {"B64_BATCH_V2": 1},
+    "mc0": {"B64_BATCH_MSG_COST": 0},
+    "mc2": {"B64_BATCH_MSG_COST": 2},
+    "mc3": {"B64_BATCH_MSG_COST": 3},
+    "mc6": {"B64_BATCH_MSG_COST": 6},
+    "mc8": {"B64_BATCH_MSG_COST": 8},
     "old_w8_c2_in4": {"B64_WARPS_C": 8, "B64_CTAS_PER_SM": 2, "B64_STAGES_IN": 4},
     "store_ef": {"B64_STORE_EVICT_FIRST": 1},
     "in3": {"B64_STAGES_IN": 3},
@@ -118,6 +131,7 @@ VARIANTS = {
     "b_p2_w32_skel": {"B64_BATCH_PASSES": 2, "B64_BATCH_WARPS": 32, "B64_SKELETON": 1},
     "b_w20": {"B64_BATCH_WARPS": 20},
     "b_trace": {"B64_BATCH_TRACE": 1},
+    "b_trace_v1": {"B64_BATCH_TRACE": 1, "B64_BATCH_V2": 0},
     "dec_stg32": {"B64_DEC_STG32": 1},
     "dec_slice": {"B64_DEC_STG32": 0},
     "dec_stg64": {"B64_DEC_STG64": 1},
