@@ -206,9 +206,10 @@ size_t b64_batch_workspace_bytes(int64_t k, int64_t total_in, int direction);
  * the device, d_in_off[0] may be > 0).  Writes d_out_off[0..k] (device,
  * d_out_off[0] = 0, d_out_off[i+1]-d_out_off[i] = b64_encoded_len(len_i))
  * and each encoding contiguously to d_out.  Messages are cut into warp
- * work units that never straddle messages, and every warp takes an equal
- * contiguous range of units -- messages are assigned to warps by the prefix
- * sums of their lengths (BASELINE.json north_star).  d_ws: b64_batch_workspace_bytes(k, total_in, 0) bytes,
+ * work units that never straddle messages, and every warp takes a
+ * contiguous range of units of equal estimated cost (a fixed part per unit
+ * plus its bytes) -- messages are assigned to warps by the prefix sums of
+ * their lengths (BASELINE.json north_star).  d_ws: b64_batch_workspace_bytes(k, total_in, 0) bytes,
  * total_in >= d_in_off[k] - d_in_off[0].  Asynchronous. */
 int b64_encode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t k, int64_t total_in,
                      uint8_t *d_out, int64_t *d_out_off, void *d_ws, size_t ws_bytes,

@@ -8,9 +8,10 @@
 // ceil(len / unit) units (at most one partial unit per message, <= 2-4 %
 // slack at data-URI sizes).  The planner scans the message lengths once
 // (output offsets + unit offsets); every warp of the persistent grid then
-// takes an equal, contiguous range of units -- i.e. messages are assigned to
-// warps by prefix-summed lengths -- gets its first message from a table the
-// plan writes and walks forward.  Warps are fully independent: each owns a
+// takes a contiguous range of units of equal estimated cost (a fixed part
+// per unit plus its bytes, B64_BATCH_UNIT_COST) -- i.e. messages are
+// assigned to warps by prefix-summed lengths -- gets its first message and
+// unit from tables the plan writes and walks forward.  Warps are fully independent: each owns a
 // 2-slot ring of 1-D TMA bulk loads (its lane 0 issues them, one mbarrier per
 // slot), a private output slice in smem, and writes its unit's output with
 // coalesced 16-byte stores (byte stores for the <16-byte unaligned edges).
