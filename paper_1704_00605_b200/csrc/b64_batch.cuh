@@ -531,10 +531,20 @@ __global__ void __launch_bounds__(kBThreads, B64_BATCH_CTAS)
 #ifdef B64_BATCH_TRACE
   unsigned long long tr_bytes = 0;
 #endif
+#ifdef B64_BATCH_TRACE_WAIT
+  unsigned long long tr_wait = 0;
+  const long long tl0 = clock64();
+#endif
   for (int32_t it = 0; it < nu; ++it) {
     const int s = it % kBSlots;
     const UnitDesc d = wc.seek(u_begin + it, k, in_off, out_off, unit_off, lane);
+#ifdef B64_BATCH_TRACE_WAIT  // measurement only: cycles spent waiting for unit data
+    const long long tw0 = clock64();
+#endif
     mbar_wait_spin(&R.full[s], static_cast<uint32_t>((it / kBSlots) & 1));
+#ifdef B64_BATCH_TRACE_WAIT
+    tr_wait += static_cast<unsigned long long>(clock64() - tw0);
+#endif
     if (it == 0) B64_TRACE(2);
 #ifdef B64_BATCH_TRACE
     tr_bytes += static_cast<unsigned long long>(d.len);
@@ -609,6 +619,12 @@ __global__ void __launch_bounds__(kBThreads, B64_BATCH_CTAS)
   if (lane == 0)
     g_trace[(blockIdx.x * 64 + warp) * 4 + 0] =
         (tr_bytes << 20) | static_cast<unsigned long long>(u_end - u_begin);
+#endif
+#ifdef B64_BATCH_TRACE_WAIT  // warps 32..: slot 0 = wait cycles, slot 1 = loop cycles
+  if (lane == 0) {
+    g_trace[(blockIdx.x * 64 + 32 + warp) * 4 + 0] = tr_wait;
+    g_trace[(blockIdx.x * 64 + 32 + warp) * 4 + 1] = static_cast<unsigned long long>(clock64() - tl0);
+  }
 #endif
   }  // u_begin < u_end
   B64_TRACE(3);

@@ -84,4 +84,5 @@
 //                        (tools/batch_trace.py); the export is not in the
 //                        header and exists only in the trace build
 //   B64_BATCH_TRACE_FM   trace stamp of each warp's first-message lookup
+//   B64_BATCH_TRACE_WAIT cycles each warp spends waiting for unit data
 //   B64_BATCH_PLAN_ONLY  the batched kernel stops after its plan

@@ -41,6 +41,11 @@ for rep in range(4):
 lib.b64_debug_trace(ctypes.addressof(buf), N)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64, 4).astype(np.int64)
 nw = int(os.environ.get("B64_TRACE_WARPS", "16"))
+if os.environ.get("B64_TRACE_WAIT"):  # batch_kernel trace-wait build: cycles waiting for unit data / in the unit loop
+    x = a[:, 32:32 + nw, :].reshape(-1, 4)
+    fr = x[:, 0] / np.maximum(x[:, 1], 1)
+    print("unit-data wait / unit loop cycles: mean", round(float(fr.mean()), 3), "p10", round(float(np.percentile(fr, 10)), 3),
+          "p90", round(float(np.percentile(fr, 90)), 3), " loop cycles p50", int(np.median(x[:, 1])))
 if os.environ.get("B64_TRACE_EXT"):  # batch2_kernel: warps 32.. hold start / searched / issued / grid-synced
     x = a[:, 32:32 + nw, :].reshape(-1, 4)
     t0x = x[:, 0].min()

@@ -132,6 +132,8 @@ VARIANTS = {
     "b_w20": {"B64_BATCH_WARPS": 20},
     "b_trace": {"B64_BATCH_TRACE": 1},
     "b_trace_v1": {"B64_BATCH_TRACE": 1, "B64_BATCH_V2": 0},
+    "b_trace_wait": {"B64_BATCH_TRACE": 1, "B64_BATCH_TRACE_WAIT": 1},
+    "b_trace_wait_s3": {"B64_BATCH_TRACE": 1, "B64_BATCH_TRACE_WAIT": 1, "B64_BATCH_SLOTS": 3},
     "dec_stg32": {"B64_DEC_STG32": 1},
     "dec_slice": {"B64_DEC_STG32": 0},
     "dec_stg64": {"B64_DEC_STG64": 1},
