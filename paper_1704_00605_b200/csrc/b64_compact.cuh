@@ -242,7 +242,9 @@ __device__ __forceinline__ void cp_load(CpSmem &S, const CpGeom &G, const uint32
 // decode (1.068 -> 1.057 ms), marginally slower in despace (0.811 vs 0.816).
 // WAITB: thread 0 waits for the reads of its earlier bulk stores (the copy-out
 // of the stream this call overwrites) just before the internal barrier.
-template <bool PIPE, bool WAITB = false>
+// NB: the internal barrier is named barrier 1 over the kCpThreads compute
+// threads (CTAs with extra producer / scan warps) instead of __syncthreads.
+template <bool PIPE, bool WAITB = false, bool NB = false>
 __device__ __forceinline__ int compact_tile(const uint8_t *win, const uint32_t *msk,
                                             uint8_t *stream, int dst, int32_t *wcnt,
                                             const uint32_t *ktab) {
@@ -272,7 +274,8 @@ __device__ __forceinline__ int compact_tile(const uint8_t *win, const uint32_t *
   const int wtot = static_cast<int>((h & 0xFFFFu) + (h >> 16));
   if (lane == 0) wcnt[warp] = wtot;
   if (WAITB && tid == 0) ptx::bulk_wait_read<0>();
-  __syncthreads();
+  if constexpr (NB) ptx::named_bar_sync(1, kCpThreads);
+  else __syncthreads();
   const int c = lane < kCpWarps ? wcnt[lane] : 0;
   int incl = c;
 #pragma unroll

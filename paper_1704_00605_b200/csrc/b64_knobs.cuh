@@ -51,6 +51,13 @@
 #define B64_BATCH_MSG_COST 4
 #endif
 
+// f3 general path: despace2_kernel (b64_despace2.cuh: one read, the
+// one-pass prefix machinery with the two-pass kernels' placement) instead of
+// cp_mask_kernel + despace_kernel.
+#ifndef B64_DS_ONEPASS2
+#define B64_DS_ONEPASS2 0
+#endif
+
 // f3 / f4 general path: the single-read kernels of b64_onepass.cuh instead
 // of the two-pass mask + compaction kernels (slower).
 #ifndef B64_CP_ONEPASS

@@ -36,8 +36,11 @@
 // (b64_compact.cuh, b64_ws.cuh).  B64_CP_ONEPASS=1 (measurement only, see
 // b64_knobs.cuh) builds the single-read kernels of b64_onepass.cuh instead;
 // measured slower on every geometry tried.
-#if B64_CP_ONEPASS
+#if B64_CP_ONEPASS || B64_DS_ONEPASS2
 #include "b64_onepass.cuh"
+#endif
+#if B64_DS_ONEPASS2
+#include "b64_despace2.cuh"
 #endif
 namespace b64 {
 constexpr size_t kDsHdrBytes = 64;  // despace workspace: WlState of the line fast path
@@ -519,6 +522,13 @@ DevInfo *device_setup_info(int *dev_out) {
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
     if (set_smem(batch2_kernel<false>, kEncRingBytes) != cudaSuccess) return nullptr;
     if (set_smem(batch2_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
+#if B64_DS_ONEPASS2 && !B64_CP_ONEPASS
+    if (set_smem(despace2_kernel, sizeof(Ds2Smem)) != cudaSuccess) return nullptr;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.op_ctas, despace2_kernel, kOpThreads,
+                                                      sizeof(Ds2Smem)) != cudaSuccess ||
+        di.op_ctas < 1)
+      return nullptr;
+#endif
 #if B64_CP_ONEPASS
     if (set_smem(despace1_kernel, sizeof(OpDsSmem)) != cudaSuccess) return nullptr;
     if (set_smem(decode_ws1_kernel, sizeof(OpWsSmem)) != cudaSuccess) return nullptr;
@@ -656,7 +666,7 @@ size_t ws_layout(int64_t k, size_t *off_units, size_t *off_done) {
   return (o + 255) & ~static_cast<size_t>(255);
 }
 
-#if B64_CP_ONEPASS
+#if B64_CP_ONEPASS || B64_DS_ONEPASS2
 int64_t op_ntiles(const void *d_in, int64_t m) {
   const int64_t imis = static_cast<int64_t>(reinterpret_cast<uintptr_t>(d_in) & 15);
   return (imis + m + kCpTile - 1) / kCpTile;
@@ -1093,6 +1103,22 @@ int b64_despace(const uint8_t *d_in, int64_t m, uint8_t *d_out, int64_t *d_out_l
   WlState *wl = reinterpret_cast<WlState *>(base);
   int64_t *counts = reinterpret_cast<int64_t *>(base + kDsHdrBytes);
   uint32_t *masks = reinterpret_cast<uint32_t *>(base + kDsHdrBytes + 8 * kCpMaxChunks);
+#if B64_DS_ONEPASS2
+  // 1. the line fast path; 2. the single-read kernel (per-tile counts in the
+  // masks' place, zeroed first), which returns at once when 1. succeeded
+  (void)counts;
+  (void)tpc;
+  (void)grid;
+  const int64_t ntiles1 = op_ntiles(d_in, m);
+  if (cudaMemsetAsync(wl, 0, sizeof(WlState), stream) != cudaSuccess ||
+      cudaMemsetAsync(masks, 0, 4 * static_cast<size_t>(ntiles1), stream) != cudaSuccess)
+    return B64_ERR_CUDA;
+  decode_lines_kernel<true><<<static_cast<unsigned>(di->sms * di->dl_ctas), kWlThreads, sizeof(WlSmemT<true>),
+                              stream>>>(d_in, m, d_out, wl, nullptr, 0, d_out_len);
+  if (cudaGetLastError() != cudaSuccess) return B64_ERR_CUDA;
+  return op_launch(despace2_kernel, ntiles1, di, sizeof(Ds2Smem), stream, d_in, m, d_out, masks,
+                   d_out_len, static_cast<const int32_t *>(&wl->verdict));
+#endif
   // 1. verified fast path for line-structured text (MIME / PEM): a strided
   // copy with the line structure checked; 2-3. the general two-pass path,
   // whose kernels return at once when 1. succeeded.

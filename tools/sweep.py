@@ -22,6 +22,9 @@ VARIANTS = {
     "base": {},
     "batch_v1": {"B64_BATCH_V2": 0},
     "uc0": {"B64_BATCH_UNIT_COST": 0},
+    "ds2": {"B64_DS_ONEPASS2": 1},
+    "ds2_l2": {"B64_DS_ONEPASS2": 1, "B64_OP_LAG": 2, "B64_OP_SLOTS": 5},
+    "ds2_l1": {"B64_DS_ONEPASS2": 1, "B64_OP_LAG": 1, "B64_OP_SLOTS": 4},
     "uc2": {"B64_BATCH_UNIT_COST": 2},
     "uc8": {"B64_BATCH_UNIT_COST": 8},
     "uc16": {"B64_BATCH_UNIT_COST": 16},
