@@ -117,3 +117,24 @@ def test_shard_key_and_combine_host():
     assert lib.b64_combine_shards(0, None, 1, 4, None) == b64.B64_ERR_ARG
     assert lib.b64_combine_shards_async(None, None, 0, 4, None, None) == b64.B64_ERR_ARG
     assert lib.b64_decode_scratch_async(None, 4, None, 0, None, None, None) == b64.B64_ERR_ARG
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: with the CUDA library absent, the binding raises on
+    the first call instead of computing anything (no oracle on the product
+    path)."""
+    import subprocess
+    import sys
+
+    code = ("import paper_1704_00605_b200 as b\n"
+            "try:\n    b.load_library()\nexcept RuntimeError as e:\n    print('RAISED', e)\n")
+    env = dict(os.environ, B64GPU_LIB=str(tmp_path / "absent.so"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=ROOT, timeout=120)
+    assert r.returncode == 0 and "RAISED" in r.stdout and "absent.so" in r.stdout, r.stdout + r.stderr
+    # the package never imports the oracle
+    pkg = os.path.join(ROOT, "paper_1704_00605_b200")
+    for f in os.listdir(pkg):
+        if f.endswith(".py"):
+            with open(os.path.join(pkg, f)) as fh:
+                assert "oracle" not in fh.read().replace("# oracle", ""), f
