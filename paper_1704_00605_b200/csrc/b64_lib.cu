@@ -25,7 +25,7 @@
 #include "b64_codec.cuh"
 #include "b64_ptx.cuh"
 #include "b64_batch.cuh"
-#include "b64_batch2.cuh"
+#include "b64_batch2.cuh"  // batch2_kernel: instantiated only with B64_BATCH_V2=1 (measurement)
 #include "b64_compact.cuh"
 #include "b64_ws.cuh"
 #include "b64_wrap.cuh"
@@ -520,8 +520,10 @@ DevInfo *device_setup_info(int *dev_out) {
     if (set_smem(encode_lines_kernel<1>, sizeof(ElSmem)) != cudaSuccess) return nullptr;
     if (set_smem(encode_lines_kernel<2>, sizeof(ElSmem)) != cudaSuccess) return nullptr;
     if (set_smem(batch_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
+#if B64_BATCH_V2
     if (set_smem(batch2_kernel<false>, kEncRingBytes) != cudaSuccess) return nullptr;
     if (set_smem(batch2_kernel<true>, kDecRingBytes) != cudaSuccess) return nullptr;
+#endif
 #if B64_DS_ONEPASS2 && !B64_CP_ONEPASS
     if (set_smem(despace2_kernel, sizeof(Ds2Smem)) != cudaSuccess) return nullptr;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di.op_ctas, despace2_kernel, kOpThreads,
