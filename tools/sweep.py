@@ -22,6 +22,12 @@ VARIANTS = {
     "base": {},
     "batch_v1": {"B64_BATCH_V2": 0},
     "uc0": {"B64_BATCH_UNIT_COST": 0},
+    "w24p5": {"B64_BATCH_WARPS": 24, "B64_BATCH_PASSES": 5},
+    "w22p5": {"B64_BATCH_WARPS": 22, "B64_BATCH_PASSES": 5},
+    "w18p7": {"B64_BATCH_WARPS": 18, "B64_BATCH_PASSES": 7},
+    "w16p8": {"B64_BATCH_WARPS": 16, "B64_BATCH_PASSES": 8},
+    "uc24": {"B64_BATCH_UNIT_COST": 24},
+    "uc12": {"B64_BATCH_UNIT_COST": 12},
     "ds2": {"B64_DS_ONEPASS2": 1},
     "ds2_l2": {"B64_DS_ONEPASS2": 1, "B64_OP_LAG": 2, "B64_OP_SLOTS": 5},
     "ds2_l1": {"B64_DS_ONEPASS2": 1, "B64_OP_LAG": 1, "B64_OP_SLOTS": 4},
